@@ -1,0 +1,967 @@
+// Host implementation of the C-ABI in include/gpuos_cuda.h.
+//
+// Owns, per GPU: the mapped-pinned task ring and its control words, the
+// device state and dual operator-table banks in HBM, the managed-memory
+// buffer arena, completion cells, and the persistent worker launch.  Every
+// CUDA call that could implicitly synchronise the device (cudaFree,
+// cudaFreeHost, module loads; profiles/r01_probe2_*.log) is kept off the
+// path that runs while the worker kernel is resident.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <immintrin.h>
+#include <nvJitLink.h>
+#include <nvrtc.h>
+#include <x86intrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "dev_common.cuh"
+#include "dev_state.h"
+#include "gpuos_cuda.h"
+
+using gdev::DevState;
+using gdev::TableEntry;
+
+namespace {
+
+uint64_t steady_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+struct BufRec {
+  void* ptr = nullptr;
+  uint64_t n = 0;
+  uint64_t bytes = 0;
+  int dtype = 0;
+  bool live = false;
+};
+
+constexpr uint32_t kBufChunkBits = 16;
+constexpr uint64_t kArenaChunk = 1ull << 30;
+
+}  // namespace
+
+struct gpuos_dev {
+  int device = 0;
+  uint32_t sms = 0;
+  gpuos_cfg cfg{};
+  cudaStream_t ks = nullptr, side = nullptr;
+  DevState* S = nullptr;
+  DevState shadow{};
+  // ring + control words (mapped pinned)
+  char* ring = nullptr;
+  uint64_t* ctl = nullptr;  // [0] tail, then done[W], claimed[W], epoch[W] (each array 128-aligned)
+  uint64_t* tail = nullptr;
+  uint64_t* mir_done = nullptr;
+  uint64_t* mir_claimed = nullptr;
+  uint64_t* mir_epoch = nullptr;
+  uint64_t cap = 0, mask = 0;
+  uint64_t reserve = 0;       // producer cursor (single producer)
+  std::atomic<uint64_t> published{0};
+  uint32_t workers = 0, threads = 0, smem = 0;
+  std::atomic<bool> running{false};
+  uint64_t last_sentinel = 0;
+  // table
+  std::mutex table_mu;
+  std::vector<TableEntry> bank[2];
+  uint64_t version = 0;
+  TableEntry* dbank[2] = {nullptr, nullptr};
+  uint64_t* dev_epoch = nullptr;
+  // buffers
+  std::mutex buf_mu;
+  std::vector<std::unique_ptr<BufRec[]>> buf_chunks;
+  uint64_t next_buf = 1;
+  char* arena_cur = nullptr;
+  uint64_t arena_left = 0;
+  std::vector<void*> managed_blocks;
+  std::unordered_map<uint64_t, std::vector<void*>> free_lists;
+  // pinned blocks and device allocations released only at close
+  std::vector<void*> pinned_blocks;
+  std::vector<void*> dev_blocks;
+  // telemetry
+  gdev::TraceRec* dtrace = nullptr;
+  uint64_t trace_cap = 0;
+  int64_t gt_offset = 0;   // host_ns = globaltimer + gt_offset
+  double tsc_per_ns = 1.0; // rdtsc -> steady ns conversion
+  uint64_t tsc0 = 0, ns0 = 0;
+  uint32_t* launch_counters = nullptr;
+  std::atomic<uint64_t> launch_seq{0};
+  int worker_regs = 0;
+  size_t worker_local = 0;
+};
+
+#define GPUOS_CK(x)                                             \
+  do {                                                          \
+    cudaError_t e_ = (x);                                       \
+    if (e_ != cudaSuccess) {                                    \
+      std::fprintf(stderr, "gpuos: %s failed: %s (%s:%d)\n", #x, \
+                   cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return GPUOS_INTERNAL;                                    \
+    }                                                           \
+  } while (0)
+
+static BufRec* buf_rec(gpuos_dev* d, uint64_t id) {
+  const uint64_t c = id >> kBufChunkBits;
+  if (id == 0 || c >= d->buf_chunks.size()) return nullptr;
+  BufRec* r = &d->buf_chunks[c][id & ((1u << kBufChunkBits) - 1)];
+  return r->live ? r : nullptr;
+}
+
+static int dev_write_field(gpuos_dev* d, size_t off, const void* src, size_t n) {
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + off, src, n, cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  return GPUOS_OK;
+}
+
+static uint64_t slot_checksum(const uint64_t* w) {
+  uint64_t h = 0;
+  for (uint32_t i = 0; i < GPUOS_SLOT_BYTES / 8; ++i)
+    if (i != 7) h += gdev::slot_mix(w[i], i);
+  return h;
+}
+
+extern "C" {
+
+int gpuos_abi_version(void) { return GPUOS_ABI_VERSION; }
+
+const char* gpuos_error_name(int c) {
+  static const char* names[] = {"Ok", "IncompatibleShapes", "OutOfBounds", "InvalidBuffer", "ZeroCapacity",
+                                "QueueFull", "ZeroSlots", "OutOfRange", "NotInstalled", "OperatorKilled",
+                                "TableFull", "SyntaxError", "UnknownIdentifier", "ArityError", "VerifyError",
+                                "EmptyAxis", "DTypeMismatch", "ShapeMismatch", "TooLarge", "OddDim",
+                                "CacheFull", "AlreadyStarted", "RuntimeStopped", "IoError", "Internal"};
+  if (c < 0 || c > 24) return "Unknown";
+  return names[c];
+}
+
+int gpuos_default_cfg(gpuos_cfg* cfg) {
+  if (!cfg) return GPUOS_INTERNAL;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->capacity = 4096;       // runtime.hpp:173
+  cfg->table_slots = 1024;    // runtime.hpp:179
+  cfg->num_workers = 0;
+  cfg->threads_per_worker = 256;
+  cfg->spin_iterations = 64;  // executor.hpp:29
+  cfg->backoff_max_exp = 6;
+  cfg->telemetry = 1;
+  cfg->yield_every = 0;
+  cfg->trace_capacity = 65536;
+  return GPUOS_OK;
+}
+
+static int calibrate_clocks(gpuos_dev* d) {
+  uint64_t* dbuf = nullptr;
+  GPUOS_CK(cudaMalloc(&dbuf, 8));
+  int64_t best_rtt = INT64_MAX;
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t h0 = steady_ns();
+    GPUOS_CK(gdev::launch_clock_probe(dbuf, d->side));
+    GPUOS_CK(cudaStreamSynchronize(d->side));
+    const uint64_t h1 = steady_ns();
+    uint64_t gt = 0;
+    GPUOS_CK(cudaMemcpy(&gt, dbuf, 8, cudaMemcpyDeviceToHost));
+    if ((int64_t)(h1 - h0) < best_rtt) {
+      best_rtt = (int64_t)(h1 - h0);
+      d->gt_offset = (int64_t)((h0 + h1) / 2) - (int64_t)gt;
+    }
+  }
+  GPUOS_CK(cudaFree(dbuf));
+  // TSC rate for cheap enqueue stamps
+  d->tsc0 = __rdtsc();
+  d->ns0 = steady_ns();
+  std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  const uint64_t t1 = __rdtsc(), n1 = steady_ns();
+  d->tsc_per_ns = (double)(t1 - d->tsc0) / (double)(n1 - d->ns0);
+  return GPUOS_OK;
+}
+
+static uint64_t tsc_to_ns(const gpuos_dev* d, uint64_t tsc) {
+  return d->ns0 + (uint64_t)((double)(int64_t)(tsc - d->tsc0) / d->tsc_per_ns);
+}
+
+static int launch_workers(gpuos_dev* d) {
+  GPUOS_CK(gdev::launch_worker(d->S, d->workers, d->threads, d->smem, d->ks));
+  d->running.store(true, std::memory_order_release);
+  return GPUOS_OK;
+}
+
+int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
+  if (!out) return GPUOS_INTERNAL;
+  *out = nullptr;
+  gpuos_cfg cfg;
+  gpuos_default_cfg(&cfg);
+  if (cfg_in) cfg = *cfg_in;
+  if (cfg.capacity == 0) return GPUOS_ZERO_CAPACITY;  // queue.hpp:163
+  if (cfg.table_slots == 0) return GPUOS_ZERO_SLOTS;  // optable.hpp:101
+  if (cfg.table_slots < GPUOS_FIRST_INJECTED_ID + 1) cfg.table_slots = GPUOS_FIRST_INJECTED_ID + 1;
+  if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 256;
+  if (cfg.threads_per_worker != 256) return GPUOS_OUT_OF_RANGE;  // worker kernel is built for 256
+  if (cfg.trace_capacity == 0) cfg.trace_capacity = 1;
+  if (cfg.backoff_max_exp > 10) cfg.backoff_max_exp = 10;
+
+  auto d = std::make_unique<gpuos_dev>();
+  d->device = device;
+  d->cfg = cfg;
+  GPUOS_CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GPUOS_CK(cudaGetDeviceProperties(&prop, device));
+  d->sms = (uint32_t)prop.multiProcessorCount;
+  // indirect calls into task bodies need a per-thread stack; set it before any
+  // kernel is resident (cudaDeviceSetLimit synchronises).
+  size_t stack = 0;
+  GPUOS_CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+  if (stack < 4096) GPUOS_CK(cudaDeviceSetLimit(cudaLimitStackSize, 4096));
+  GPUOS_CK(cudaStreamCreateWithFlags(&d->ks, cudaStreamNonBlocking));
+  GPUOS_CK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+  gdev::load_all_kernels(&d->worker_regs, &d->worker_local);
+  GPUOS_CK(cudaGetLastError());
+
+  d->threads = cfg.threads_per_worker;
+  d->smem = gdev::worker_smem_bytes();
+  d->workers = cfg.num_workers ? cfg.num_workers : d->sms;
+  if (d->workers > gdev::kMaxWorkers) d->workers = gdev::kMaxWorkers;
+
+  // ring capacity: power of two, min 2 (queue.hpp:164-165)
+  uint64_t cap = 2;
+  while (cap < cfg.capacity) cap <<= 1;
+  d->cap = cap;
+  d->mask = cap - 1;
+
+  // mapped pinned memory: control words + ring
+  const size_t W = d->workers;
+  const size_t mir_words = ((W + 15) / 16) * 16;
+  const size_t ctl_bytes = 128 + 3 * mir_words * 8;
+  void* ctl = nullptr;
+  GPUOS_CK(cudaHostAlloc(&ctl, ctl_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(ctl, 0, ctl_bytes);
+  d->pinned_blocks.push_back(ctl);
+  d->ctl = (uint64_t*)ctl;
+  d->tail = d->ctl;
+  d->mir_done = d->ctl + 16;
+  d->mir_claimed = d->mir_done + mir_words;
+  d->mir_epoch = d->mir_claimed + mir_words;
+  for (size_t i = 0; i < W; ++i) d->mir_epoch[i] = gdev::kQuiescent;
+  void* ring = nullptr;
+  GPUOS_CK(cudaHostAlloc(&ring, cap * GPUOS_SLOT_BYTES, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(ring, 0, cap * GPUOS_SLOT_BYTES);
+  d->pinned_blocks.push_back(ring);
+  d->ring = (char*)ring;
+  for (uint64_t i = 0; i < cap; ++i) *(uint64_t*)(d->ring + i * GPUOS_SLOT_BYTES) = i;  // slot i free for lap 0
+
+  // device state
+  GPUOS_CK(cudaMalloc(&d->S, sizeof(DevState)));
+  GPUOS_CK(cudaMalloc(&d->dbank[0], cfg.table_slots * sizeof(TableEntry)));
+  GPUOS_CK(cudaMalloc(&d->dbank[1], cfg.table_slots * sizeof(TableEntry)));
+  GPUOS_CK(cudaMemset(d->dbank[0], 0, cfg.table_slots * sizeof(TableEntry)));
+  GPUOS_CK(cudaMemset(d->dbank[1], 0, cfg.table_slots * sizeof(TableEntry)));
+  d->bank[0].assign(cfg.table_slots, TableEntry{});
+  d->bank[1].assign(cfg.table_slots, TableEntry{});
+  GPUOS_CK(cudaMalloc(&d->dev_epoch, W * 8));
+  GPUOS_CK(cudaMemset(d->dev_epoch, 0xff, W * 8));
+  d->trace_cap = cfg.trace_capacity;
+  GPUOS_CK(cudaMalloc(&d->dtrace, d->trace_cap * sizeof(gdev::TraceRec)));
+  GPUOS_CK(cudaMemset(d->dtrace, 0, d->trace_cap * sizeof(gdev::TraceRec)));
+  GPUOS_CK(cudaMalloc(&d->launch_counters, gdev::kLaunchCounters * 4));
+  GPUOS_CK(cudaMemset(d->launch_counters, 0, gdev::kLaunchCounters * 4));
+
+  DevState& s = d->shadow;
+  std::memset(&s, 0, sizeof(s));
+  s.stop_pos = gdev::kRunning;
+  s.yield_every = cfg.yield_every;
+  s.trace_on = cfg.telemetry ? 1 : 0;
+  s.spin_iterations = cfg.spin_iterations ? cfg.spin_iterations : 1;
+  s.backoff_max_exp = cfg.backoff_max_exp;
+  s.bank[0] = d->dbank[0];
+  s.bank[1] = d->dbank[1];
+  s.bank_gen[0] = 0;
+  s.bank_gen[1] = 0;
+  s.table_slots = cfg.table_slots;
+  s.num_workers = d->workers;
+  void* dp = nullptr;
+  GPUOS_CK(cudaHostGetDevicePointer(&dp, ring, 0));
+  s.ring = (gpuos_task*)dp;
+  s.cap = cap;
+  s.mask = cap - 1;
+  GPUOS_CK(cudaHostGetDevicePointer(&dp, ctl, 0));
+  uint64_t* dctl = (uint64_t*)dp;
+  s.host_tail = dctl;
+  s.host_done = dctl + 16;
+  s.host_claimed = s.host_done + mir_words;
+  s.host_epoch = s.host_claimed + mir_words;
+  s.dev_epoch = d->dev_epoch;
+  s.trace = d->dtrace;
+  s.trace_cap = d->trace_cap;
+  GPUOS_CK(cudaMemcpy(d->S, &s, sizeof(s), cudaMemcpyHostToDevice));
+
+  int rc = calibrate_clocks(d.get());
+  if (rc) return rc;
+  GPUOS_CK(cudaDeviceSynchronize());
+  rc = launch_workers(d.get());
+  if (rc) return rc;
+  *out = d.release();
+  return GPUOS_OK;
+}
+
+// Commit the shutdown sentinel behind all published work (executor.hpp:119-128)
+// and wait for the kernel to drain and exit.
+int gpuos_dev_stop(gpuos_dev* d) {
+  if (!d) return GPUOS_INTERNAL;
+  if (!d->running.load(std::memory_order_acquire)) return GPUOS_OK;
+  uint64_t pos = 0;
+  for (;;) {
+    if (gpuos_ring_reserve(d, &pos) == GPUOS_OK) break;
+    std::this_thread::yield();  // workers are draining; a slot will free up
+  }
+  gpuos_task t;
+  std::memset(&t, 0, sizeof(t));
+  t.flags = GPUOS_FLAG_SHUTDOWN;
+  gpuos_ring_publish(d, pos, &t);
+  d->last_sentinel = pos;
+  GPUOS_CK(cudaSetDevice(d->device));
+  GPUOS_CK(cudaStreamSynchronize(d->ks));
+  d->running.store(false, std::memory_order_release);
+  return GPUOS_OK;
+}
+
+int gpuos_dev_start(gpuos_dev* d) {
+  if (!d) return GPUOS_INTERNAL;
+  if (d->running.load(std::memory_order_acquire)) return GPUOS_ALREADY_STARTED;
+  GPUOS_CK(cudaSetDevice(d->device));
+  // resume right after the consumed sentinel: tickets past it were abandoned
+  const uint64_t next = d->last_sentinel + 1;
+  DevState& s = d->shadow;
+  s.claim = next;
+  s.hint = next;
+  s.stop_pos = gdev::kRunning;
+  int rc = dev_write_field(d, offsetof(DevState, claim), &s.claim, 8);
+  if (!rc) rc = dev_write_field(d, offsetof(DevState, hint), &s.hint, 8);
+  if (!rc) rc = dev_write_field(d, offsetof(DevState, stop_pos), &s.stop_pos, 8);
+  if (rc) return rc;
+  return launch_workers(d);
+}
+
+int gpuos_dev_close(gpuos_dev* d) {
+  if (!d) return GPUOS_OK;
+  gpuos_dev_stop(d);
+  cudaSetDevice(d->device);
+  cudaDeviceSynchronize();
+  cudaFree(d->S);
+  cudaFree(d->dbank[0]);
+  cudaFree(d->dbank[1]);
+  cudaFree(d->dev_epoch);
+  cudaFree(d->dtrace);
+  cudaFree(d->launch_counters);
+  for (void* p : d->dev_blocks) cudaFree(p);
+  for (void* p : d->managed_blocks) cudaFree(p);
+  for (void* p : d->pinned_blocks) cudaFreeHost(p);
+  cudaStreamDestroy(d->ks);
+  cudaStreamDestroy(d->side);
+  delete d;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_alive(gpuos_dev* d) {
+  if (!d || !d->running.load(std::memory_order_acquire)) return 0;
+  cudaSetDevice(d->device);
+  return cudaStreamQuery(d->ks) == cudaErrorNotReady ? 1 : 0;
+}
+
+int gpuos_dev_num_workers(gpuos_dev* d, uint32_t* n) {
+  if (!d || !n) return GPUOS_INTERNAL;
+  *n = d->workers;
+  return GPUOS_OK;
+}
+
+int gpuos_dev_sm_count(gpuos_dev* d, uint32_t* n) {
+  if (!d || !n) return GPUOS_INTERNAL;
+  *n = d->sms;
+  return GPUOS_OK;
+}
+
+int gpuos_set_yield_every(gpuos_dev* d, uint64_t n) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  d->shadow.yield_every = n;
+  return dev_write_field(d, offsetof(DevState, yield_every), &n, 8);
+}
+
+int gpuos_dev_clock_offset(gpuos_dev* d, int64_t* off) {
+  if (!d || !off) return GPUOS_INTERNAL;
+  *off = d->gt_offset;
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- buffers
+
+int gpuos_buf_alloc(gpuos_dev* d, int dtype, uint64_t n, uint64_t* id, void** ptr) {
+  if (!d || !id) return GPUOS_INTERNAL;
+  if (dtype < 0 || dtype > GPUOS_BF16) return GPUOS_DTYPE_MISMATCH;
+  cudaSetDevice(d->device);
+  const uint64_t raw = n * (uint64_t)gdev::dtype_width(dtype);
+  const uint64_t bytes = ((raw ? raw : 1) + 255) & ~255ull;
+  std::lock_guard<std::mutex> lk(d->buf_mu);
+  void* p = nullptr;
+  auto fl = d->free_lists.find(bytes);
+  if (fl != d->free_lists.end() && !fl->second.empty()) {
+    p = fl->second.back();
+    fl->second.pop_back();
+  } else if (bytes > kArenaChunk / 4) {
+    GPUOS_CK(cudaMallocManaged(&p, bytes));
+    d->managed_blocks.push_back(p);
+  } else {
+    if (d->arena_left < bytes) {
+      void* blk = nullptr;
+      GPUOS_CK(cudaMallocManaged(&blk, kArenaChunk));
+      d->managed_blocks.push_back(blk);
+      d->arena_cur = (char*)blk;
+      d->arena_left = kArenaChunk;
+    }
+    p = d->arena_cur;
+    d->arena_cur += bytes;
+    d->arena_left -= bytes;
+  }
+  // zero-filled (tensor.hpp:272-273), on the device so the pages start in HBM
+  GPUOS_CK(cudaMemsetAsync(p, 0, bytes, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  const uint64_t bid = d->next_buf++;
+  const uint64_t c = bid >> kBufChunkBits;
+  while (d->buf_chunks.size() <= c) d->buf_chunks.emplace_back(new BufRec[1u << kBufChunkBits]);
+  BufRec& r = d->buf_chunks[c][bid & ((1u << kBufChunkBits) - 1)];
+  r.ptr = p;
+  r.n = n;
+  r.bytes = bytes;
+  r.dtype = dtype;
+  r.live = true;
+  *id = bid;
+  if (ptr) *ptr = p;
+  return GPUOS_OK;
+}
+
+// Ids are never reused (tensor.hpp:257-258); storage goes to a free list
+// because cudaFree would block behind the resident worker kernel.
+int gpuos_buf_free(gpuos_dev* d, uint64_t id) {
+  if (!d) return GPUOS_INTERNAL;
+  std::lock_guard<std::mutex> lk(d->buf_mu);
+  BufRec* r = buf_rec(d, id);
+  if (!r) return GPUOS_INVALID_BUFFER;
+  r->live = false;
+  d->free_lists[r->bytes].push_back(r->ptr);
+  return GPUOS_OK;
+}
+
+int gpuos_buf_lookup(gpuos_dev* d, uint64_t id, int* dtype, uint64_t* n, void** ptr) {
+  if (!d) return GPUOS_INTERNAL;
+  std::lock_guard<std::mutex> lk(d->buf_mu);
+  BufRec* r = buf_rec(d, id);
+  if (!r) return GPUOS_INVALID_BUFFER;
+  if (dtype) *dtype = r->dtype;
+  if (n) *n = r->n;
+  if (ptr) *ptr = r->ptr;
+  return GPUOS_OK;
+}
+
+int gpuos_buf_copy(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int dir) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  const cudaMemcpyKind k = dir == 0 ? cudaMemcpyHostToDevice : dir == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  GPUOS_CK(cudaMemcpyAsync(dst, src, bytes, k, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  return GPUOS_OK;
+}
+
+int gpuos_buf_prefetch(gpuos_dev* d, uint64_t id) {
+  if (!d) return GPUOS_INTERNAL;
+  void* p = nullptr;
+  uint64_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(d->buf_mu);
+    BufRec* r = buf_rec(d, id);
+    if (!r) return GPUOS_INVALID_BUFFER;
+    p = r->ptr;
+    bytes = r->bytes;
+  }
+  cudaSetDevice(d->device);
+  cudaMemLocation loc{};
+  loc.type = cudaMemLocationTypeDevice;
+  loc.id = d->device;
+  GPUOS_CK(cudaMemPrefetchAsync(p, bytes, loc, 0, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  return GPUOS_OK;
+}
+
+int gpuos_view_bind(gpuos_dev* d, uint64_t id, int dtype, int64_t offset, int rank, const int64_t* ext,
+                    const int64_t* str, gpuos_view* out) {
+  if (!d || !out) return GPUOS_INTERNAL;
+  std::memset(out, 0, sizeof(*out));
+  if (rank < 0 || rank > GPUOS_MAX_RANK) return GPUOS_TOO_LARGE;
+  out->dtype = (uint8_t)dtype;
+  out->rank = (uint8_t)rank;
+  out->buffer_lo = (uint32_t)id;
+  int64_t lo = offset, hi = offset, n = 1;
+  for (int i = 0; i < rank; ++i) {
+    if (ext[i] > INT32_MAX || ext[i] < 0 || str[i] > INT32_MAX || str[i] < INT32_MIN) return GPUOS_TOO_LARGE;
+    out->extents[i] = (int32_t)ext[i];
+    out->strides[i] = (int32_t)str[i];
+    n *= ext[i];
+    if (ext[i] > 0) {
+      if (str[i] > 0) hi += (ext[i] - 1) * str[i];
+      else lo += (ext[i] - 1) * str[i];
+    }
+  }
+  std::lock_guard<std::mutex> lk(d->buf_mu);
+  BufRec* r = buf_rec(d, id);
+  if (!r) {
+    out->status = GPUOS_VIEW_UNKNOWN_BUFFER;
+    return GPUOS_OK;
+  }
+  if (r->dtype != dtype) {
+    out->status = GPUOS_VIEW_DTYPE_VS_BUFFER;
+    return GPUOS_OK;
+  }
+  if (n > 0 && (lo < 0 || hi >= (int64_t)r->n)) {
+    out->status = GPUOS_VIEW_OUT_OF_BOUNDS;
+    return GPUOS_OK;
+  }
+  out->addr = (uint64_t)((char*)r->ptr + offset * gdev::dtype_width(dtype));
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- cells
+
+int gpuos_cells_alloc(gpuos_dev* d, uint64_t count, uint64_t** host, uint64_t* device_addr) {
+  if (!d || !host || count == 0) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  void* p = nullptr;
+  GPUOS_CK(cudaHostAlloc(&p, count * 8, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(p, 0, count * 8);
+  void* dp = nullptr;
+  GPUOS_CK(cudaHostGetDevicePointer(&dp, p, 0));
+  {
+    std::lock_guard<std::mutex> lk(d->buf_mu);
+    d->pinned_blocks.push_back(p);
+  }
+  *host = (uint64_t*)p;
+  if (device_addr) *device_addr = (uint64_t)dp;
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- ring
+
+int gpuos_ring_capacity(gpuos_dev* d, uint64_t* c) {
+  if (!d || !c) return GPUOS_INTERNAL;
+  *c = d->cap;
+  return GPUOS_OK;
+}
+
+int gpuos_ring_reserve(gpuos_dev* d, uint64_t* pos) {
+  const uint64_t p = d->reserve;
+  const uint64_t* w = (const uint64_t*)(d->ring + (p & d->mask) * GPUOS_SLOT_BYTES);
+  if (__atomic_load_n(w, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
+  d->reserve = p + 1;
+  *pos = p;
+  _mm_prefetch(d->ring + ((p + 8) & d->mask) * GPUOS_SLOT_BYTES, _MM_HINT_T0);
+  return GPUOS_OK;
+}
+
+int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
+  alignas(64) uint64_t w[GPUOS_SLOT_BYTES / 8];
+  std::memcpy(w, task, GPUOS_SLOT_BYTES);
+  w[0] = pos + 1;
+  if (d->shadow.trace_on) w[5] = __rdtsc();  // enqueue stamp, converted at trace export
+  w[7] = 0;
+  w[7] = slot_checksum(w);
+  char* dst = d->ring + (pos & d->mask) * GPUOS_SLOT_BYTES;
+  // body with streaming stores, then the publication word after a fence, then the tail
+  for (int i = 1; i < GPUOS_SLOT_BYTES / 16; ++i)
+    _mm_stream_si128((__m128i*)(dst + 16 * i), _mm_load_si128((const __m128i*)((const char*)w + 16 * i)));
+  _mm_sfence();
+  __atomic_store_n((uint64_t*)(dst + 8), w[1], __ATOMIC_RELAXED);
+  __atomic_store_n((uint64_t*)dst, w[0], __ATOMIC_RELEASE);
+  __atomic_store_n(d->tail, pos + 1, __ATOMIC_RELEASE);
+  d->published.store(pos + 1, std::memory_order_relaxed);
+  return GPUOS_OK;
+}
+
+static uint64_t sum_mirror(const gpuos_dev* d, const uint64_t* m) {
+  uint64_t s = 0;
+  for (uint32_t i = 0; i < d->workers; ++i) s += __atomic_load_n(&m[i], __ATOMIC_ACQUIRE);
+  return s;
+}
+
+int gpuos_ring_peek(gpuos_dev* d, gpuos_snapshot* s) {
+  if (!d || !s) return GPUOS_INTERNAL;
+  // processed, then head, then tail: each mirror is monotone and written
+  // claimed-before-done, so processed <= head <= tail holds.
+  s->processed = sum_mirror(d, d->mir_done);
+  s->head = sum_mirror(d, d->mir_claimed);
+  s->tail = __atomic_load_n(d->tail, __ATOMIC_ACQUIRE);
+  return GPUOS_OK;
+}
+
+int gpuos_ring_wait_processed(gpuos_dev* d, uint64_t count) {
+  if (!d) return GPUOS_INTERNAL;
+  uint32_t spins = 0;
+  while (sum_mirror(d, d->mir_done) < count) {
+    if (!d->running.load(std::memory_order_acquire)) return GPUOS_RUNTIME_STOPPED;
+    if (++spins < 64) {
+      _mm_pause();
+    } else if (spins < 256) {
+      std::this_thread::yield();
+    } else {
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      if ((spins & 1023) == 0 && !gpuos_dev_alive(d)) return GPUOS_INTERNAL;
+    }
+  }
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- table
+
+int gpuos_table_slots(gpuos_dev* d, uint32_t* n) {
+  if (!d || !n) return GPUOS_INTERNAL;
+  *n = d->cfg.table_slots;
+  return GPUOS_OK;
+}
+
+int gpuos_table_version(gpuos_dev* d, uint64_t* v) {
+  if (!d || !v) return GPUOS_INTERNAL;
+  std::lock_guard<std::mutex> lk(d->table_mu);
+  *v = d->version;
+  return GPUOS_OK;
+}
+
+int gpuos_table_status(gpuos_dev* d, uint32_t op_id, int* status, int* kind) {
+  if (!d) return GPUOS_INTERNAL;
+  if (op_id >= d->cfg.table_slots) return GPUOS_OUT_OF_RANGE;
+  std::lock_guard<std::mutex> lk(d->table_mu);
+  const TableEntry& e = d->bank[d->version & 1][op_id];
+  if (status) *status = e.status;
+  if (kind) *kind = e.kind;
+  return GPUOS_OK;
+}
+
+// Block until no worker can still dispatch from a snapshot older than
+// `required`; quiescent workers are skipped (optable.hpp:591-600).
+static uint64_t wait_for_epochs(gpuos_dev* d, uint64_t required) {
+  const uint64_t t0 = steady_ns();
+  if (!d->running.load(std::memory_order_acquire)) return 0;
+  for (uint32_t i = 0; i < d->workers; ++i) {
+    uint32_t spins = 0;
+    for (;;) {
+      const uint64_t e = __atomic_load_n(&d->mir_epoch[i], __ATOMIC_ACQUIRE);
+      if (e == gdev::kQuiescent || e >= required) break;
+      if (!d->running.load(std::memory_order_acquire)) break;
+      if (++spins > 64) std::this_thread::yield();
+      else _mm_pause();
+    }
+  }
+  return steady_ns() - t0;
+}
+
+// Rebuild the inactive bank from the active one, apply, stamp the generation,
+// publish with a version store (optable.hpp:197-234).
+static int table_mutate(gpuos_dev* d, uint32_t op_id, const TableEntry& ent, gpuos_inject_stats* st) {
+  if (op_id >= d->cfg.table_slots) return GPUOS_OUT_OF_RANGE;
+  cudaSetDevice(d->device);
+  std::lock_guard<std::mutex> lk(d->table_mu);
+  const uint64_t v = d->version;
+  const uint64_t wait_ns = wait_for_epochs(d, v);
+  const uint64_t t0 = steady_ns();
+  const int nb = (int)((v + 1) & 1);
+  d->bank[nb] = d->bank[v & 1];
+  d->bank[nb][op_id] = ent;
+  GPUOS_CK(cudaMemcpyAsync(d->dbank[nb], d->bank[nb].data(), d->bank[nb].size() * sizeof(TableEntry),
+                           cudaMemcpyHostToDevice, d->side));
+  d->shadow.bank_gen[nb] = v + 1;
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, bank_gen) + nb * 8, &d->shadow.bank_gen[nb], 8,
+                           cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  const uint64_t t1 = steady_ns();
+  const uint64_t nv = v + 1;
+  d->shadow.version = nv;
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, version), &d->shadow.version, 8,
+                           cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  d->version = nv;
+  if (st) {
+    st->epoch_wait_ns = wait_ns;
+    st->bank_write_ns = t1 - t0;
+    st->flip_ns = steady_ns() - t1;
+    st->version = nv;
+  }
+  return GPUOS_OK;
+}
+
+int gpuos_table_install_builtin(gpuos_dev* d, uint32_t op_id, uint32_t kind) {
+  if (!d) return GPUOS_INTERNAL;
+  if (kind >= GPUOS_NUM_BUILTINS) return GPUOS_NOT_INSTALLED;
+  TableEntry e{};
+  e.kind = (uint16_t)kind;
+  e.status = 1;
+  return table_mutate(d, op_id, e, nullptr);
+}
+
+int gpuos_table_install_program(gpuos_dev* d, uint32_t op_id, const gpuos_instr* code, uint32_t n_instr,
+                                int arity, int dtype, gpuos_inject_stats* st) {
+  if (!d || !code) return GPUOS_INTERNAL;
+  if (op_id >= d->cfg.table_slots) return GPUOS_OUT_OF_RANGE;
+  if (n_instr == 0 || n_instr > GPUOS_MAX_PROGRAM) return GPUOS_VERIFY_ERROR;
+  if (arity < 0 || arity > GPUOS_MAX_INPUTS) return GPUOS_ARITY_ERROR;
+  // device-side verification bound: the interpreter stack is GPUOS_MAX_STACK deep
+  int depth = 0, maxd = 0;
+  for (uint32_t i = 0; i < n_instr; ++i) {
+    const int op = code[i].op;
+    if (op == GPUOS_BC_PUSH_CONST || op == GPUOS_BC_LOAD_IN) {
+      if (op == GPUOS_BC_LOAD_IN && (code[i].k < 0 || code[i].k >= arity)) return GPUOS_VERIFY_ERROR;
+      ++depth;
+    } else if (op == GPUOS_BC_ADD || op == GPUOS_BC_SUB || op == GPUOS_BC_MUL || op == GPUOS_BC_DIV ||
+               op == GPUOS_BC_MAX || op == GPUOS_BC_MIN) {
+      if (depth < 2) return GPUOS_VERIFY_ERROR;
+      --depth;
+    } else if (op == GPUOS_BC_STORE_OUT) {
+      if (i + 1 != n_instr || depth != 1) return GPUOS_VERIFY_ERROR;
+      --depth;
+    } else if (op > GPUOS_BC_STORE_OUT) {
+      return GPUOS_VERIFY_ERROR;
+    } else if (depth < 1) {
+      return GPUOS_VERIFY_ERROR;
+    }
+    maxd = std::max(maxd, depth);
+  }
+  if (maxd > GPUOS_MAX_STACK) return GPUOS_VERIFY_ERROR;
+  cudaSetDevice(d->device);
+  const uint64_t t0 = steady_ns();
+  const size_t bytes = sizeof(gdev::ProgramHeader) + n_instr * sizeof(gpuos_instr);
+  std::vector<char> img(bytes);
+  gdev::ProgramHeader h{n_instr, arity, dtype, maxd};
+  std::memcpy(img.data(), &h, sizeof(h));
+  std::memcpy(img.data() + sizeof(h), code, n_instr * sizeof(gpuos_instr));
+  void* p = nullptr;
+  GPUOS_CK(cudaMalloc(&p, bytes));
+  GPUOS_CK(cudaMemcpyAsync(p, img.data(), bytes, cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  {
+    std::lock_guard<std::mutex> lk(d->buf_mu);
+    d->dev_blocks.push_back(p);  // programs live for the process
+  }
+  const uint64_t t1 = steady_ns();
+  TableEntry e{};
+  e.kind = GPUOS_KIND_PROGRAM;
+  e.status = 1;
+  e.aux = (uint64_t)p;
+  const int rc = table_mutate(d, op_id, e, st);
+  if (st) st->upload_ns = t1 - t0;
+  return rc;
+}
+
+int gpuos_table_kill(gpuos_dev* d, uint32_t op_id) {
+  if (!d) return GPUOS_INTERNAL;
+  TableEntry e{};
+  e.kind = GPUOS_KIND_KILLED;
+  e.status = 2;
+  return table_mutate(d, op_id, e, nullptr);
+}
+
+// ---------------------------------------------------------------- telemetry
+
+int gpuos_dev_get_stats(gpuos_dev* d, gpuos_dev_stats* out) {
+  if (!d || !out) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  DevState tmp;
+  GPUOS_CK(cudaMemcpyAsync(&tmp, d->S, sizeof(DevState), cudaMemcpyDeviceToHost, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  out->processed = tmp.processed;
+  out->failed = tmp.failed;
+  out->canary_hits = tmp.canary_hits;
+  out->stalls = tmp.stalls;
+  out->torn_reads = tmp.torn_reads;
+  std::memcpy(out->per_op, tmp.per_op, sizeof(out->per_op));
+  return GPUOS_OK;
+}
+
+int gpuos_trace_enable(gpuos_dev* d, int on) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  d->shadow.trace_on = on ? 1u : 0u;
+  return dev_write_field(d, offsetof(DevState, trace_on), &d->shadow.trace_on, 4);
+}
+
+int gpuos_trace_snapshot(gpuos_dev* d, gpuos_tracepoint* out, uint64_t cap, uint64_t* n) {
+  if (!d || !n) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  uint64_t head = 0;
+  GPUOS_CK(cudaMemcpyAsync(&head, (char*)d->S + offsetof(DevState, trace_head), 8, cudaMemcpyDeviceToHost, d->side));
+  std::vector<gdev::TraceRec> recs(d->trace_cap);
+  GPUOS_CK(cudaMemcpyAsync(recs.data(), d->dtrace, d->trace_cap * sizeof(gdev::TraceRec), cudaMemcpyDeviceToHost,
+                           d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  const uint64_t have = std::min<uint64_t>(head, d->trace_cap);
+  uint64_t k = 0;
+  for (uint64_t ticket = head - have; ticket < head && k < cap; ++ticket) {
+    const gdev::TraceRec& r = recs[ticket % d->trace_cap];
+    if (r.stamp != ticket * 2 + 2) continue;  // in progress or overwritten
+    gpuos_tracepoint& tp = out[k++];
+    tp.seq = r.seq;
+    tp.op_id = r.op_id;
+    tp.worker = (uint32_t)r.worker;
+    tp.reserved = 0;
+    tp.enqueue_ns = tsc_to_ns(d, r.enqueue_ns);
+    const uint64_t deq = (uint64_t)((int64_t)r.dequeue_gt + d->gt_offset);
+    tp.dequeue_ns = deq >= tp.enqueue_ns ? deq : tp.enqueue_ns;  // executor.hpp:246
+    tp.exec_ns = r.exec_ns;
+    tp.version = r.version;
+  }
+  *n = k;
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- conventional path
+
+static uint32_t parts_for(const gpuos_dev* d, const gpuos_task* t, uint32_t kind) {
+  const gpuos_view& o = t->views[0];
+  int64_t n = 1;
+  for (int i = 0; i < o.rank; ++i) n *= o.extents[i];
+  int64_t p = 1;
+  switch (kind) {
+    case GPUOS_OP_ADD: case GPUOS_OP_MUL: case GPUOS_OP_RELU: case GPUOS_OP_GELU: case GPUOS_KIND_PROGRAM:
+      p = (n + 2047) / 2048;
+      break;
+    case GPUOS_OP_SOFTMAX: case GPUOS_OP_LAYERNORM: case GPUOS_OP_REDUCE_SUM: case GPUOS_OP_REDUCE_MAX:
+    case GPUOS_OP_REDUCE_MIN: {
+      const gpuos_view& in = t->views[1];
+      int64_t rows = 1;
+      for (int i = 0; i + 1 < in.rank; ++i) rows *= in.extents[i];
+      p = (rows + 7) / 8;
+      break;
+    }
+    case GPUOS_OP_MATMUL_SMALL:
+      if (o.rank == 2) p = (int64_t)((o.extents[0] + 63) / 64) * ((o.extents[1] + 63) / 64);
+      break;
+    case GPUOS_OP_VECMAT: p = (n + 255) / 256; break;
+    case GPUOS_OP_SDPA: p = o.rank >= 1 ? o.extents[0] : 1; break;
+    case GPUOS_OP_ROPE: p = (n / 2 + 2047) / 2048; break;
+    default: p = 1;
+  }
+  const int64_t maxp = 4 * (int64_t)d->sms;
+  if (p < 1) p = 1;
+  if (p > maxp) p = maxp;
+  return (uint32_t)p;
+}
+
+int gpuos_launch_task(gpuos_dev* d, const gpuos_task* t, void* stream) {
+  if (!d || !t) return GPUOS_INTERNAL;
+  if (t->op_id >= d->cfg.table_slots) return GPUOS_OUT_OF_RANGE;
+  TableEntry e;
+  {
+    std::lock_guard<std::mutex> lk(d->table_mu);
+    e = d->bank[d->version & 1][t->op_id];
+  }
+  if (e.status == 0) return GPUOS_NOT_INSTALLED;
+  if (e.status == 2) return GPUOS_OPERATOR_KILLED;
+  cudaSetDevice(d->device);
+  const uint32_t nparts = parts_for(d, t, e.kind);
+  uint32_t* counter = d->launch_counters + (d->launch_seq.fetch_add(1, std::memory_order_relaxed) % gdev::kLaunchCounters);
+  cudaStream_t st = stream ? (cudaStream_t)stream : d->side;
+  GPUOS_CK(gdev::launch_task(t, e.kind, e.aux, nparts, counter, st));
+  return GPUOS_OK;
+}
+
+int gpuos_stream_create(gpuos_dev* d, void** stream) {
+  if (!d || !stream) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  cudaStream_t s;
+  GPUOS_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *stream = (void*)s;
+  return GPUOS_OK;
+}
+
+int gpuos_stream_sync(gpuos_dev* d, void* stream) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaStreamSynchronize(stream ? (cudaStream_t)stream : d->side));
+  return GPUOS_OK;
+}
+
+int gpuos_stream_destroy(gpuos_dev* d, void* stream) {
+  if (!d || !stream) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaStreamDestroy((cudaStream_t)stream));
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- NVRTC / nvJitLink
+
+int gpuos_jit_compile(const char* src, const char* const* opts, int nopts, void** cubin, size_t* size,
+                      uint64_t* compile_ns, uint64_t* link_ns, char* log, size_t logcap) {
+  if (!src || !cubin || !size) return GPUOS_INTERNAL;
+  auto put_log = [&](const std::string& s) {
+    if (log && logcap) {
+      std::snprintf(log, logcap, "%s", s.c_str());
+    }
+  };
+  const uint64_t t0 = steady_ns();
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src, "gpuos_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return GPUOS_INTERNAL;
+  std::vector<const char*> o;
+  o.push_back("-arch=sm_100a");
+  o.push_back("-rdc=true");
+  o.push_back("--fmad=false");
+  for (int i = 0; i < nopts; ++i) o.push_back(opts[i]);
+  const nvrtcResult r = nvrtcCompileProgram(prog, (int)o.size(), o.data());
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string l(n, '\0');
+    nvrtcGetProgramLog(prog, l.data());
+    put_log(l);
+    nvrtcDestroyProgram(&prog);
+    return GPUOS_SYNTAX_ERROR;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> relo(n);
+  nvrtcGetCUBIN(prog, relo.data());
+  nvrtcDestroyProgram(&prog);
+  const uint64_t t1 = steady_ns();
+  nvJitLinkHandle h;
+  const char* lopts[] = {"-arch=sm_100a"};
+  if (nvJitLinkCreate(&h, 1, lopts) != NVJITLINK_SUCCESS) return GPUOS_INTERNAL;
+  if (nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, relo.data(), relo.size(), "gpuos_jit") != NVJITLINK_SUCCESS ||
+      nvJitLinkComplete(h) != NVJITLINK_SUCCESS) {
+    size_t ln = 0;
+    nvJitLinkGetErrorLogSize(h, &ln);
+    std::string l(ln, '\0');
+    nvJitLinkGetErrorLog(h, l.data());
+    put_log(l);
+    nvJitLinkDestroy(&h);
+    return GPUOS_VERIFY_ERROR;
+  }
+  size_t cs = 0;
+  nvJitLinkGetLinkedCubinSize(h, &cs);
+  void* out = std::malloc(cs);
+  nvJitLinkGetLinkedCubin(h, out);
+  nvJitLinkDestroy(&h);
+  const uint64_t t2 = steady_ns();
+  *cubin = out;
+  *size = cs;
+  if (compile_ns) *compile_ns = t1 - t0;
+  if (link_ns) *link_ns = t2 - t1;
+  return GPUOS_OK;
+}
+
+void gpuos_free(void* p) { std::free(p); }
+
+}  // extern "C"

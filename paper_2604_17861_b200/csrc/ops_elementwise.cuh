@@ -1,0 +1,325 @@
+// Elementwise task bodies: add / mul / relu / gelu (reference ops.hpp:133-194),
+// the injected-operator stack machine (bytecode.hpp:205-230 evaluated by
+// opcompiler.hpp:70-122's broadcast driver) and kv_append (ops.hpp:544-589).
+//
+// Every body evaluates in double and narrows once on store, like the
+// reference's BoundView path, so f32/f16/bf16/i32 add/mul/relu are bit-exact.
+// The dense path moves 16 bytes per operand per thread with four independent
+// vectors in flight; the strided/broadcast path walks a coalesced rank<=4
+// space with fast divmod.
+#pragma once
+
+#include "dev_common.cuh"
+#include "dev_state.h"
+
+namespace gdev {
+
+// ---- scalar functions in reference evaluation order (no contraction) ----
+struct FAdd {
+  static constexpr int A = 2;
+  __device__ __forceinline__ double operator()(const double* v) const { return __dadd_rn(v[0], v[1]); }
+};
+struct FMul {
+  static constexpr int A = 2;
+  __device__ __forceinline__ double operator()(const double* v) const { return __dmul_rn(v[0], v[1]); }
+};
+struct FRelu {
+  static constexpr int A = 1;
+  // v < 0 ? 0 : v keeps -0.0 and NaN (ops.hpp:188)
+  __device__ __forceinline__ double operator()(const double* v) const { return v[0] < 0.0 ? 0.0 : v[0]; }
+};
+struct FGelu {
+  static constexpr int A = 1;
+  // 0.5 * x * (1 + tanh(c * (x + 0.044715 * x * x * x))), c = sqrt(2/pi)  (ops.hpp:79-82)
+  __device__ __forceinline__ double operator()(const double* v) const {
+    const double x = v[0];
+    const double c = 0x1.9884533d43651p-1;  // sqrt(2.0 / pi) as glibc computes it
+    const double x3 = __dmul_rn(__dmul_rn(__dmul_rn(0.044715, x), x), x);
+    const double inner = __dmul_rn(c, __dadd_rn(x, x3));
+    return __dmul_rn(__dmul_rn(0.5, x), __dadd_rn(1.0, tanh(inner)));
+  }
+};
+
+// ---- the shared elementwise driver ----
+template <int DT, class F>
+__device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int64_t n, F f) {
+  typedef typename DT_<DT>::T T;
+  constexpr int A = F::A;
+  T* out = (T*)t->views[0].addr;
+  const T* in[A];
+#pragma unroll
+  for (int k = 0; k < A; ++k) in[k] = (const T*)t->views[1 + k].addr;
+  bool aligned = ((uintptr_t)out & 15) == 0;
+#pragma unroll
+  for (int k = 0; k < A; ++k) aligned = aligned && (((uintptr_t)in[k] & 15) == 0);
+  constexpr int V = 16 / sizeof(T);
+  constexpr int U = 4;
+  int64_t tail_lo = 0;
+  if (aligned) {
+    const int64_t nv = n / V;
+    int64_t lo, hi;
+    part_range(nv, c->part, c->nparts, 1, &lo, &hi);
+    const int stride = c->nthreads;
+    for (int64_t i0 = lo + c->tid; i0 < hi; i0 += (int64_t)stride * U) {
+      uint4 vin[A][U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + (int64_t)u * stride;
+        if (i < hi) {
+#pragma unroll
+          for (int k = 0; k < A; ++k) vin[k][u] = ld_cg_v4(reinterpret_cast<const uint4*>(in[k]) + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + (int64_t)u * stride;
+        if (i < hi) {
+          uint4 vo;
+          const T* ev[A];
+#pragma unroll
+          for (int k = 0; k < A; ++k) ev[k] = reinterpret_cast<const T*>(&vin[k][u]);
+          T* eo = reinterpret_cast<T*>(&vo);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            double x[A];
+#pragma unroll
+            for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(ev[k] + j);
+            DT_<DT>::store(eo + j, f(x));
+          }
+          reinterpret_cast<uint4*>(out)[i] = vo;
+        }
+      }
+    }
+    if (c->part != c->nparts - 1) return;  // the last partition owns the scalar tail
+    tail_lo = nv * V;
+  } else {
+    int64_t lo, hi;
+    part_range(n, c->part, c->nparts, 1, &lo, &hi);
+    for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
+      double x[A];
+#pragma unroll
+      for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + e);
+      DT_<DT>::store(out + e, f(x));
+    }
+    return;
+  }
+  for (int64_t e = tail_lo + c->tid; e < n; e += c->nthreads) {
+    double x[A];
+#pragma unroll
+    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + e);
+    DT_<DT>::store(out + e, f(x));
+  }
+}
+
+template <int DT, class F>
+__device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, const Space& s,
+                                           int64_t n, F f) {
+  typedef typename DT_<DT>::T T;
+  constexpr int A = F::A;
+  T* out = (T*)t->views[0].addr;
+  const T* in[A];
+#pragma unroll
+  for (int k = 0; k < A; ++k) in[k] = (const T*)t->views[1 + k].addr;
+  int64_t lo, hi;
+  part_range(n, c->part, c->nparts, 1, &lo, &hi);
+  for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
+    int64_t off[1 + A];
+    space_offsets(s, (uint32_t)e, off);
+    double x[A];
+#pragma unroll
+    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + off[1 + k]);
+    DT_<DT>::store(out + off[0], f(x));
+  }
+}
+
+// Checks in the reference order (ops.hpp:133-153), then dispatch on dtype.
+template <class F>
+__device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
+  constexpr int A = F::A;
+  if (t->n_inputs != A) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  if (!allow_int && out.dtype == GPUOS_I32) return GPUOS_DTYPE_MISMATCH;
+  for (int k = 0; k < A; ++k)
+    if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  const int64_t n = numel(out);
+  if (n == 0) return GPUOS_OK;
+  if (n >= (int64_t)1 << 31) return GPUOS_TOO_LARGE;
+  int64_t st[A][GPUOS_MAX_RANK];
+  for (int k = 0; k < A; ++k) {
+    if (!broadcast_strides(t->views[1 + k], out, st[k])) return GPUOS_INCOMPATIBLE_SHAPES;
+    const int b = bind_code(t->views[1 + k]);
+    if (b) return b;
+  }
+  const int b = bind_code(out);
+  if (b) return b;
+  Space s;
+  build_space(s, out, A, st);
+  F f;
+  switch (out.dtype) {
+#define GPUOS_EW_CASE(DT)                        \
+  case DT:                                       \
+    if (s.dense)                                 \
+      ew_dense<DT>(t, c, n, f);                  \
+    else                                         \
+      ew_strided<DT>(t, c, s, n, f);             \
+    break;
+    GPUOS_EW_CASE(GPUOS_F32)
+    GPUOS_EW_CASE(GPUOS_F64)
+    GPUOS_EW_CASE(GPUOS_I32)
+    GPUOS_EW_CASE(GPUOS_F16)
+    GPUOS_EW_CASE(GPUOS_BF16)
+#undef GPUOS_EW_CASE
+    default: return GPUOS_DTYPE_MISMATCH;
+  }
+  return GPUOS_OK;
+}
+
+__device__ __noinline__ int op_add(const gpuos_task* t, const Ctx* c) { return ew_body<FAdd>(t, c, true); }
+__device__ __noinline__ int op_mul(const gpuos_task* t, const Ctx* c) { return ew_body<FMul>(t, c, true); }
+__device__ __noinline__ int op_relu(const gpuos_task* t, const Ctx* c) { return ew_body<FRelu>(t, c, true); }
+__device__ __noinline__ int op_gelu(const gpuos_task* t, const Ctx* c) { return ew_body<FGelu>(t, c, false); }
+
+// ---------------------------------------------------------------------------
+// Injected operators: a verified stack-machine program evaluated in double per
+// element over broadcast inputs.  Program layout in HBM: ProgramHeader then
+// n_instr gpuos_instr.  (Live injection path: no module load.)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double run_program(const gpuos_instr* code, int n_instr, const double* in) {
+  double stack[GPUOS_MAX_STACK];
+  int sp = 0;
+  for (int pc = 0; pc < n_instr; ++pc) {
+    const gpuos_instr ins = code[pc];
+    switch (ins.op) {
+      case GPUOS_BC_PUSH_CONST: stack[sp++] = ins.value; break;
+      case GPUOS_BC_LOAD_IN: stack[sp++] = in[ins.k]; break;
+      case GPUOS_BC_ADD: --sp; stack[sp - 1] = __dadd_rn(stack[sp - 1], stack[sp]); break;
+      case GPUOS_BC_SUB: --sp; stack[sp - 1] = __dsub_rn(stack[sp - 1], stack[sp]); break;
+      case GPUOS_BC_MUL: --sp; stack[sp - 1] = __dmul_rn(stack[sp - 1], stack[sp]); break;
+      case GPUOS_BC_DIV: --sp; stack[sp - 1] = __ddiv_rn(stack[sp - 1], stack[sp]); break;
+      case GPUOS_BC_NEG: stack[sp - 1] = -stack[sp - 1]; break;
+      case GPUOS_BC_EXP: stack[sp - 1] = exp(stack[sp - 1]); break;
+      case GPUOS_BC_TANH: stack[sp - 1] = tanh(stack[sp - 1]); break;
+      case GPUOS_BC_MAX: {  // binop_max: a < b ? b : a (expr.hpp:134)
+        --sp;
+        const double a = stack[sp - 1], b = stack[sp];
+        stack[sp - 1] = a < b ? b : a;
+        break;
+      }
+      case GPUOS_BC_MIN: {  // binop_min: b < a ? b : a (expr.hpp:135)
+        --sp;
+        const double a = stack[sp - 1], b = stack[sp];
+        stack[sp - 1] = b < a ? b : a;
+        break;
+      }
+      case GPUOS_BC_ABS: stack[sp - 1] = fabs(stack[sp - 1]); break;
+      case GPUOS_BC_SQRT: stack[sp - 1] = __dsqrt_rn(stack[sp - 1]); break;
+      case GPUOS_BC_NARROW: stack[sp - 1] = narrow_any(ins.k, stack[sp - 1]); break;
+      default: return stack[sp - 1];  // STORE_OUT
+    }
+  }
+  return stack[sp > 0 ? sp - 1 : 0];
+}
+
+template <int DT>
+__device__ void program_loop(const gpuos_task* t, const Ctx* c, const Space& s, int64_t n,
+                             const gpuos_instr* code, int n_instr, int arity) {
+  typedef typename DT_<DT>::T T;
+  T* out = (T*)t->views[0].addr;
+  const T* in[GPUOS_MAX_INPUTS];
+  for (int k = 0; k < arity; ++k) in[k] = (const T*)t->views[1 + k].addr;
+  int64_t lo, hi;
+  part_range(n, c->part, c->nparts, 1, &lo, &hi);
+  for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
+    int64_t off[1 + GPUOS_MAX_INPUTS];
+    if (s.dense) {
+      for (int k = 0; k <= arity; ++k) off[k] = e;
+    } else {
+      space_offsets(s, (uint32_t)e, off);
+    }
+    double x[GPUOS_MAX_INPUTS];
+    for (int k = 0; k < arity; ++k) x[k] = DT_<DT>::load(in[k] + off[1 + k]);
+    DT_<DT>::store(out + off[0], run_program(code, n_instr, x));
+  }
+}
+
+// Checks in load_module's order (opcompiler.hpp:72-101).
+__device__ __noinline__ int op_program(const gpuos_task* t, const Ctx* c) {
+  const ProgramHeader* h = (const ProgramHeader*)c->aux;
+  if (h == nullptr) return GPUOS_VERIFY_ERROR;
+  const int arity = h->arity;
+  if (t->n_inputs != arity) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  if (out.dtype != h->dtype) return GPUOS_DTYPE_MISMATCH;
+  const int64_t n = numel(out);
+  if (n == 0) return GPUOS_OK;
+  if (n >= (int64_t)1 << 31) return GPUOS_TOO_LARGE;
+  int64_t st[GPUOS_MAX_INPUTS][GPUOS_MAX_RANK];
+  for (int k = 0; k < arity; ++k) {
+    if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+    if (!broadcast_strides(t->views[1 + k], out, st[k])) return GPUOS_INCOMPATIBLE_SHAPES;
+    const int b = bind_code(t->views[1 + k]);
+    if (b) return b;
+  }
+  const int b = bind_code(out);
+  if (b) return b;
+  Space s;
+  build_space(s, out, arity, st);
+  // stage the program in shared memory (<= GPUOS_MAX_PROGRAM instructions)
+  const int n_instr = (int)h->n_instr;
+  gpuos_instr* code = (gpuos_instr*)c->smem;
+  const gpuos_instr* src = (const gpuos_instr*)(h + 1);
+  for (int i = c->tid; i < n_instr; i += c->nthreads) code[i] = src[i];
+  group_sync(c);
+  switch (out.dtype) {
+    case GPUOS_F32: program_loop<GPUOS_F32>(t, c, s, n, code, n_instr, arity); break;
+    case GPUOS_F64: program_loop<GPUOS_F64>(t, c, s, n, code, n_instr, arity); break;
+    case GPUOS_I32: program_loop<GPUOS_I32>(t, c, s, n, code, n_instr, arity); break;
+    case GPUOS_F16: program_loop<GPUOS_F16>(t, c, s, n, code, n_instr, arity); break;
+    case GPUOS_BF16: program_loop<GPUOS_BF16>(t, c, s, n, code, n_instr, arity); break;
+    default: break;
+  }
+  group_sync(c);  // program scratch is reused by the next task
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kv_append: inputs {new_k, new_v, v_cache}, output k_cache, scalars[0] = cursor
+// (ops.hpp:544-589).  A bit-exact copy through the double load/store path.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ int op_kv_append(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 3) return GPUOS_ARITY_ERROR;
+  if (t->n_scalars == 0) return GPUOS_ARITY_ERROR;
+  const gpuos_view& kc = t->views[0];
+  const gpuos_view& nk = t->views[1];
+  const gpuos_view& nv = t->views[2];
+  const gpuos_view& vc = t->views[3];
+  if (kc.rank != 3 || vc.rank != 3 || nk.rank != 2 || nv.rank != 2) return GPUOS_SHAPE_MISMATCH;
+  const int h = kc.extents[0], cap = kc.extents[1], d = kc.extents[2];
+  if (!same_shape(vc, kc)) return GPUOS_SHAPE_MISMATCH;
+  if (nk.extents[0] != h || nk.extents[1] != d || nv.extents[0] != h || nv.extents[1] != d)
+    return GPUOS_SHAPE_MISMATCH;
+  if (nk.dtype != kc.dtype || nv.dtype != vc.dtype || vc.dtype != kc.dtype) return GPUOS_DTYPE_MISMATCH;
+  const double cs = t->scalars[0];
+  // static_cast<int64_t>(double): truncation; NaN/out-of-range land outside [0, cap)
+  const int64_t cursor = (cs > -9.2e18 && cs < 9.2e18) ? (int64_t)cs : (int64_t)-1;
+  if (cursor < 0 || cursor >= cap) return GPUOS_CACHE_FULL;
+  int b;
+  if ((b = bind_code(kc)) || (b = bind_code(vc)) || (b = bind_code(nk)) || (b = bind_code(nv))) return b;
+  const int dt = kc.dtype;
+  const int64_t total = (int64_t)h * d;
+  int64_t lo, hi;
+  part_range(total, c->part, c->nparts, 1, &lo, &hi);
+  for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
+    const int64_t head = e / d, j = e % d;
+    const int64_t ko = head * kc.strides[0] + cursor * kc.strides[1] + j * kc.strides[2];
+    const int64_t vo = head * vc.strides[0] + cursor * vc.strides[1] + j * vc.strides[2];
+    const int64_t no = head * nk.strides[0] + j * nk.strides[1];
+    const int64_t mo = head * nv.strides[0] + j * nv.strides[1];
+    store_any(dt, (char*)kc.addr, ko, load_any(dt, (const char*)nk.addr, no));
+    store_any(dt, (char*)vc.addr, vo, load_any(dt, (const char*)nv.addr, mo));
+  }
+  return GPUOS_OK;
+}
+
+}  // namespace gdev

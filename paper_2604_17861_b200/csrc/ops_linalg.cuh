@@ -1,0 +1,296 @@
+// Matrix and attention task bodies on CUDA cores in fp64: matmul_small /
+// vecmat (reference ops.hpp:363-433), single-query sdpa (ops.hpp:441-498) and
+// rope (ops.hpp:503-537).
+//
+// Accumulation order matches the reference exactly (ascending k, one rounding
+// per product and per add).  For f32/f16/bf16 operands every product is exact
+// in fp64, so a DFMA equals the reference's separate multiply and add and is
+// used; f64/i32 operands use __dmul_rn + __dadd_rn.  The bf16/f16 tensor-core
+// (tcgen05) GEMM lives in ops_umma.cuh.
+#pragma once
+
+#include "dev_common.cuh"
+
+namespace gdev {
+
+__device__ __forceinline__ bool exact_products(int dt) {
+  return dt == GPUOS_F32 || dt == GPUOS_F16 || dt == GPUOS_BF16;
+}
+__device__ __forceinline__ double mac(double acc, double a, double b, bool exact) {
+  return exact ? fma(a, b, acc) : __dadd_rn(acc, __dmul_rn(a, b));
+}
+
+// ---- matmul: a (m,k) x b (k,n) -> out (m,n) ----
+constexpr int kTM = 64, kTN = 64, kTK = 32;
+
+__device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 2) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& a = t->views[1];
+  const gpuos_view& b = t->views[2];
+  if (a.dtype != out.dtype || b.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (a.rank != 2 || b.rank != 2 || out.rank != 2) return GPUOS_SHAPE_MISMATCH;
+  const int m = a.extents[0], k = a.extents[1], n = b.extents[1];
+  if (b.extents[0] != k) return GPUOS_SHAPE_MISMATCH;
+  if (out.extents[0] != m || out.extents[1] != n) return GPUOS_SHAPE_MISMATCH;
+  if (!(c->flags & GPUOS_FLAG_UNCAPPED) &&
+      (m > GPUOS_SMALL_MATMUL_MAX_DIM || k > GPUOS_SMALL_MATMUL_MAX_DIM || n > GPUOS_SMALL_MATMUL_MAX_DIM))
+    return GPUOS_TOO_LARGE;
+  int bc;
+  if ((bc = bind_code(a)) || (bc = bind_code(b)) || (bc = bind_code(out))) return bc;
+  const int dt = out.dtype;
+  const bool exact = exact_products(dt);
+  const char* ap = (const char*)a.addr;
+  const char* bp = (const char*)b.addr;
+  char* op = (char*)out.addr;
+  const int64_t sa0 = a.strides[0], sa1 = a.strides[1], sb0 = b.strides[0], sb1 = b.strides[1];
+  const int64_t so0 = out.strides[0], so1 = out.strides[1];
+  double* As = (double*)c->smem;             // [kTM][kTK+1]
+  double* Bs = As + kTM * (kTK + 1);         // [kTK][kTN+1]
+  const int ntm = (m + kTM - 1) / kTM, ntn = (n + kTN - 1) / kTN;
+  int64_t tlo, thi;
+  part_range((int64_t)ntm * ntn, c->part, c->nparts, 1, &tlo, &thi);
+  const int nt = c->nthreads;
+  // 256 threads: 16x16 grid, 4x4 outputs each (rows ty+16r, cols tx+16q)
+  const int ty = c->tid >> 4, tx = c->tid & 15;
+  const bool grid16 = (nt == 256);
+  for (int64_t tile = tlo; tile < thi; ++tile) {
+    const int i0 = (int)(tile / ntn) * kTM, j0 = (int)(tile % ntn) * kTN;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
+    for (int k0 = 0; k0 < k; k0 += kTK) {
+      for (int e = c->tid; e < kTM * kTK; e += nt) {
+        const int i = e / kTK, kk = e % kTK;
+        const int gi = i0 + i, gk = k0 + kk;
+        As[i * (kTK + 1) + kk] = (gi < m && gk < k) ? load_any(dt, ap, gi * sa0 + gk * sa1) : 0.0;
+      }
+      for (int e = c->tid; e < kTK * kTN; e += nt) {
+        const int kk = e / kTN, j = e % kTN;
+        const int gk = k0 + kk, gj = j0 + j;
+        Bs[kk * (kTN + 1) + j] = (gk < k && gj < n) ? load_any(dt, bp, gk * sb0 + gj * sb1) : 0.0;
+      }
+      group_sync(c);
+      const int kmax = (k - k0) < kTK ? (k - k0) : kTK;
+      if (grid16) {
+        for (int kk = 0; kk < kmax; ++kk) {
+          double av[4], bv[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) av[r] = As[(ty + 16 * r) * (kTK + 1) + kk];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bv[q] = Bs[kk * (kTN + 1) + tx + 16 * q];
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[r][q] = mac(acc[r][q], av[r], bv[q], exact);
+        }
+      } else {
+        // generic group size: each thread owns tile elements e = tid + nt*s (s < 16)
+        for (int s = 0; s < 16; ++s) {
+          const int e = c->tid + nt * s;
+          if (e >= kTM * kTN) break;
+          const int i = e / kTN, j = e % kTN;
+          double v = acc[s >> 2][s & 3];
+          for (int kk = 0; kk < kmax; ++kk) v = mac(v, As[i * (kTK + 1) + kk], Bs[kk * (kTN + 1) + j], exact);
+          acc[s >> 2][s & 3] = v;
+        }
+      }
+      group_sync(c);
+    }
+    if (grid16) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int gi = i0 + ty + 16 * r, gj = j0 + tx + 16 * q;
+          if (gi < m && gj < n) store_any(dt, op, gi * so0 + gj * so1, acc[r][q]);
+        }
+    } else {
+      for (int s = 0; s < 16; ++s) {
+        const int e = c->tid + nt * s;
+        if (e >= kTM * kTN) break;
+        const int gi = i0 + e / kTN, gj = j0 + e % kTN;
+        if (gi < m && gj < n) store_any(dt, op, gi * so0 + gj * so1, acc[s >> 2][s & 3]);
+      }
+    }
+  }
+  return GPUOS_OK;
+}
+
+// ---- vecmat: v (k) x mat (k,n) -> out (n) ----
+__device__ __noinline__ int op_vecmat(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 2) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& v = t->views[1];
+  const gpuos_view& mt = t->views[2];
+  if (v.dtype != out.dtype || mt.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (v.rank != 1 || mt.rank != 2 || out.rank != 1) return GPUOS_SHAPE_MISMATCH;
+  const int k = v.extents[0], n = mt.extents[1];
+  if (mt.extents[0] != k || out.extents[0] != n) return GPUOS_SHAPE_MISMATCH;
+  if (!(c->flags & GPUOS_FLAG_UNCAPPED) && (k > GPUOS_SMALL_MATMUL_MAX_DIM || n > GPUOS_SMALL_MATMUL_MAX_DIM))
+    return GPUOS_TOO_LARGE;
+  int bc;
+  if ((bc = bind_code(v)) || (bc = bind_code(mt)) || (bc = bind_code(out))) return bc;
+  const int dt = out.dtype;
+  const bool exact = exact_products(dt);
+  int64_t lo, hi;
+  part_range(n, c->part, c->nparts, 1, &lo, &hi);
+  for (int64_t j = lo + c->tid; j < hi; j += c->nthreads) {
+    double acc = 0.0;
+    for (int p = 0; p < k; ++p)
+      acc = mac(acc, load_any(dt, (const char*)v.addr, (int64_t)p * v.strides[0]),
+                load_any(dt, (const char*)mt.addr, (int64_t)p * mt.strides[0] + j * mt.strides[1]), exact);
+    store_any(dt, (char*)out.addr, j * out.strides[0], acc);
+  }
+  return GPUOS_OK;
+}
+
+// ---- sdpa: q (h,d), k (h,t,d), v (h,t,d) -> out (h,d) ----
+__device__ __forceinline__ double nan_skip_max(double a, double b) {
+  if (b != b) return a;
+  if (a != a) return b;
+  return a < b ? b : a;
+}
+
+__device__ __noinline__ int op_sdpa(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 3) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& q = t->views[1];
+  const gpuos_view& kk = t->views[2];
+  const gpuos_view& vv = t->views[3];
+  if (!is_float_dt(out.dtype)) return GPUOS_DTYPE_MISMATCH;
+  if (q.dtype != out.dtype || kk.dtype != out.dtype || vv.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (q.rank != 2 || kk.rank != 3 || vv.rank != 3) return GPUOS_SHAPE_MISMATCH;
+  const int h = q.extents[0], d = q.extents[1], tl = kk.extents[1];
+  if (kk.extents[0] != h || kk.extents[2] != d || !same_shape(vv, kk)) return GPUOS_SHAPE_MISMATCH;
+  if (!same_shape(out, q)) return GPUOS_SHAPE_MISMATCH;
+  if (tl == 0) return GPUOS_EMPTY_AXIS;
+  const double scale = (t->n_scalars > 0 && t->scalars[0] > 0.0) ? t->scalars[0]
+                                                                  : __ddiv_rn(1.0, __dsqrt_rn((double)d));
+  int bc;
+  if ((bc = bind_code(q)) || (bc = bind_code(kk)) || (bc = bind_code(vv)) || (bc = bind_code(out))) return bc;
+  const int dt = out.dtype;
+  const bool exact = exact_products(dt);
+  double* red = (double*)c->smem;           // 32 doubles
+  double* sc = red + 32;                    // score chunk
+  const int cap = (c->smem_bytes - 32 * 8) / 8;
+  const int chunk = cap < tl ? cap : tl;
+  const bool single = chunk >= tl;
+  int64_t hlo, hhi;
+  part_range(h, c->part, c->nparts, 1, &hlo, &hhi);
+  const char* qp = (const char*)q.addr;
+  const char* kp = (const char*)kk.addr;
+  const char* vp = (const char*)vv.addr;
+  for (int64_t head = hlo; head < hhi; ++head) {
+    const int64_t qb = head * q.strides[0], kb = head * kk.strides[0], vb = head * vv.strides[0];
+    auto score = [&](int i) {
+      double dot = 0.0;
+      for (int j = 0; j < d; ++j)
+        dot = mac(dot, load_any(dt, qp, qb + (int64_t)j * q.strides[1]),
+                  load_any(dt, kp, kb + (int64_t)i * kk.strides[1] + (int64_t)j * kk.strides[2]), exact);
+      return __dmul_rn(scale, dot);
+    };
+    // pass 1: max score
+    double mx = -INFINITY;
+    for (int i = c->tid; i < tl; i += c->nthreads) {
+      const double s = score(i);
+      if (single) sc[i] = s;
+      mx = nan_skip_max(mx, s);
+    }
+    {
+      for (int o = 16; o > 0; o >>= 1) mx = nan_skip_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((c->tid & 31) == 0) red[c->tid >> 5] = mx;
+      group_sync(c);
+      mx = -INFINITY;
+      for (int w = 0; w < (c->nthreads >> 5); ++w) mx = nan_skip_max(mx, red[w]);
+      group_sync(c);
+    }
+    // pass 2: denominator
+    double s = 0.0;
+    for (int i = c->tid; i < tl; i += c->nthreads) {
+      const double e = exp(__dsub_rn(single ? sc[i] : score(i), mx));
+      if (single) sc[i] = e;
+      s += e;
+    }
+    const double denom = group_sum(s, c, red);
+    // pass 3: out[j] = sum_i (e_i / denom) * v[i][j], ascending i
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i0 = 0; i0 < tl; i0 += chunk) {
+      const int i1 = (i0 + chunk) < tl ? (i0 + chunk) : tl;
+      if (!single) {
+        for (int i = i0 + c->tid; i < i1; i += c->nthreads) sc[i - i0] = exp(__dsub_rn(score(i), mx));
+        group_sync(c);
+      }
+      for (int r = 0; r < 4; ++r) {
+        const int j = c->tid + r * c->nthreads;
+        if (j >= d) break;
+        double a = acc[r];
+        for (int i = i0; i < i1; ++i) {
+          const double w = __ddiv_rn(sc[i - (single ? 0 : i0)], denom);
+          a = __dadd_rn(a, __dmul_rn(w, load_any(dt, vp, vb + (int64_t)i * vv.strides[1] + (int64_t)j * vv.strides[2])));
+        }
+        acc[r] = a;
+      }
+      group_sync(c);
+    }
+    for (int r = 0; r < 4; ++r) {
+      const int j = c->tid + r * c->nthreads;
+      if (j >= d) break;
+      store_any(dt, (char*)out.addr, head * out.strides[0] + (int64_t)j * out.strides[1], acc[r]);
+    }
+    if (d > 4 * c->nthreads) {
+      // very wide heads: remaining columns, recomputing weights from scores
+      for (int j = c->tid + 4 * c->nthreads; j < d; j += c->nthreads) {
+        double a = 0.0;
+        for (int i = 0; i < tl; ++i) {
+          const double e = single ? sc[i] : exp(__dsub_rn(score(i), mx));
+          a = __dadd_rn(a, __dmul_rn(__ddiv_rn(e, denom),
+                                     load_any(dt, vp, vb + (int64_t)i * vv.strides[1] + (int64_t)j * vv.strides[2])));
+        }
+        store_any(dt, (char*)out.addr, head * out.strides[0] + (int64_t)j * out.strides[1], a);
+      }
+    }
+    group_sync(c);
+  }
+  return GPUOS_OK;
+}
+
+// ---- rope: x (t,d), positions (t) -> out (t,d) ----
+__device__ __noinline__ int op_rope(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 2) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& x = t->views[1];
+  const gpuos_view& pos = t->views[2];
+  if (!is_float_dt(out.dtype)) return GPUOS_DTYPE_MISMATCH;
+  if (x.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (x.rank != 2 || pos.rank != 1) return GPUOS_SHAPE_MISMATCH;
+  if (!same_shape(out, x)) return GPUOS_SHAPE_MISMATCH;
+  const int tl = x.extents[0], d = x.extents[1];
+  if (pos.extents[0] != tl) return GPUOS_SHAPE_MISMATCH;
+  if (d % 2 != 0) return GPUOS_ODD_DIM;
+  const double base = (t->n_scalars > 0 && t->scalars[0] > 0.0) ? t->scalars[0] : 10000.0;
+  int bc;
+  if ((bc = bind_code(x)) || (bc = bind_code(pos)) || (bc = bind_code(out))) return bc;
+  const int dt = out.dtype;
+  const int half = d / 2;
+  int64_t lo, hi;
+  part_range((int64_t)tl * half, c->part, c->nparts, 1, &lo, &hi);
+  for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
+    const int64_t r = e / half, i = e % half;
+    const double p = load_any(pos.dtype, (const char*)pos.addr, r * pos.strides[0]);
+    const double ex = __ddiv_rn(__dmul_rn(-2.0, (double)i), (double)d);
+    const double theta = __dmul_rn(p, pow(base, ex));
+    double sn, cs;
+    sincos(theta, &sn, &cs);
+    const int64_t xb = r * x.strides[0], ob = r * out.strides[0];
+    const double x0 = load_any(dt, (const char*)x.addr, xb + (2 * i) * x.strides[1]);
+    const double x1 = load_any(dt, (const char*)x.addr, xb + (2 * i + 1) * x.strides[1]);
+    store_any(dt, (char*)out.addr, ob + (2 * i) * out.strides[1], __dsub_rn(__dmul_rn(x0, cs), __dmul_rn(x1, sn)));
+    store_any(dt, (char*)out.addr, ob + (2 * i + 1) * out.strides[1], __dadd_rn(__dmul_rn(x0, sn), __dmul_rn(x1, cs)));
+  }
+  return GPUOS_OK;
+}
+
+}  // namespace gdev

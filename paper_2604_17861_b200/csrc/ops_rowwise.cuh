@@ -1,0 +1,309 @@
+// Row-wise task bodies over the last axis: softmax (reference ops.hpp:200-238),
+// layernorm (ops.hpp:244-294) and the sum/max/min reduction (ops.hpp:303-355).
+//
+// Rows of <= 1024 elements go one warp per row; longer rows use the whole
+// worker group.  Sums accumulate in fp64 (the reference's accumulation type)
+// with a shuffle tree; max/min carry (value, index) pairs so the result is
+// the first extremum in scan order, and a NaN first element wins exactly as
+// the reference's `acc < x` scan does.
+#pragma once
+
+#include "dev_common.cuh"
+
+namespace gdev {
+
+// Outer (all-but-last) iteration over a view: rank-1 <= 3 dims.
+struct RowIter {
+  int r;                  // outer rank
+  int32_t ext[3];
+  FastDiv fd[3];
+  int64_t rows;
+  __device__ __forceinline__ void init(const gpuos_view& v) {
+    r = v.rank - 1;
+    rows = 1;
+    for (int d = 0; d < r; ++d) {
+      ext[d] = v.extents[d];
+      fd[d].init((uint32_t)(ext[d] > 0 ? ext[d] : 1));
+      rows *= ext[d];
+    }
+  }
+  // element offset of row `row` in a view whose first r strides are `st`
+  __device__ __forceinline__ void offsets(int64_t row, const int32_t* st_a, const int32_t* st_b,
+                                          int64_t* oa, int64_t* ob) const {
+    uint32_t e = (uint32_t)row;
+    int64_t a = 0, b = 0;
+    for (int d = r - 1; d >= 0; --d) {
+      const uint32_t q = fd[d].div(e);
+      const uint32_t i = e - q * fd[d].d;
+      e = q;
+      a += (int64_t)i * st_a[d];
+      b += (int64_t)i * st_b[d];
+    }
+    *oa = a;
+    *ob = b;
+  }
+};
+
+// Distribution of rows over the group: warp-per-row when cols are short.
+struct RowSched {
+  bool per_warp;
+  int unit;      // this thread's unit index (warp or 0)
+  int nunits;    // units per group
+  int lane;      // index within the unit
+  int width;     // threads per unit
+  int64_t lo, hi;
+  __device__ __forceinline__ void init(const Ctx* c, int64_t rows, int64_t cols) {
+    per_warp = cols <= 1024;
+    if (per_warp) {
+      unit = c->tid >> 5;
+      nunits = c->nthreads >> 5;
+      lane = c->tid & 31;
+      width = 32;
+    } else {
+      unit = 0;
+      nunits = 1;
+      lane = c->tid;
+      width = c->nthreads;
+    }
+    part_range(rows, c->part, c->nparts, 1, &lo, &hi);
+  }
+};
+
+// Sum over one unit; for the whole-group unit this synchronises the group.
+__device__ __forceinline__ double unit_sum(double v, const RowSched& rs, const Ctx* c, double* red) {
+  if (rs.per_warp) return warp_sum(v);
+  return group_sum(v, c, red);
+}
+__device__ __forceinline__ double unit_max(double v, const RowSched& rs, const Ctx* c, double* red) {
+  if (rs.per_warp) return warp_max(v);
+  return group_max(v, c, red);
+}
+
+// First-wins extremum with NaN-skipping, as a (value, index) pair.
+struct Ext {
+  double v;
+  int64_t i;  // -1 => no candidate
+};
+__device__ __forceinline__ Ext ext_merge(Ext a, Ext b, bool is_max) {
+  if (a.i < 0) return b;
+  if (b.i < 0) return a;
+  const bool b_better = is_max ? (a.v < b.v) : (b.v < a.v);
+  const bool a_better = is_max ? (b.v < a.v) : (a.v < b.v);
+  if (b_better) return b;
+  if (a_better) return a;
+  return a.i <= b.i ? a : b;  // equal under ==: the earlier element wins
+}
+__device__ __forceinline__ Ext warp_ext(Ext e, bool is_max) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Ext x;
+    x.v = __shfl_xor_sync(0xffffffffu, e.v, o);
+    x.i = __shfl_xor_sync(0xffffffffu, e.i, o);
+    e = ext_merge(e, x, is_max);
+  }
+  return e;
+}
+__device__ __forceinline__ Ext unit_ext(Ext e, bool is_max, const RowSched& rs, const Ctx* c, char* scratch) {
+  e = warp_ext(e, is_max);
+  if (rs.per_warp) return e;
+  double* rv = (double*)scratch;
+  int64_t* ri = (int64_t*)(scratch + 32 * sizeof(double));
+  const int lane = c->tid & 31, wid = c->tid >> 5, nw = c->nthreads >> 5;
+  if (lane == 0) {
+    rv[wid] = e.v;
+    ri[wid] = e.i;
+  }
+  group_sync(c);
+  Ext t;
+  t.v = rv[0];
+  t.i = ri[0];
+  for (int w = 1; w < nw; ++w) {
+    Ext x;
+    x.v = rv[w];
+    x.i = ri[w];
+    t = ext_merge(t, x, is_max);
+  }
+  group_sync(c);
+  return t;
+}
+
+// Row maximum with the reference's scan semantics (NaN first element => NaN).
+__device__ __forceinline__ double row_max_scan(int dt, const char* base, int64_t step, int64_t cols,
+                                               const RowSched& rs, const Ctx* c, char* scratch) {
+  Ext e;
+  e.v = 0.0;
+  e.i = -1;
+  for (int64_t j = rs.lane; j < cols; j += rs.width) {
+    const double x = load_any(dt, base, j * step);
+    if (x == x) {
+      Ext y;
+      y.v = x;
+      y.i = j;
+      e = ext_merge(e, y, true);
+    }
+  }
+  e = unit_ext(e, true, rs, c, scratch);
+  const double x0 = load_any(dt, base, 0);
+  return (x0 != x0) ? x0 : e.v;
+}
+
+// ---- softmax ----
+__device__ __noinline__ int op_softmax(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& in = t->views[1];
+  if (!is_float_dt(out.dtype)) return GPUOS_DTYPE_MISMATCH;
+  if (in.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (!same_shape(in, out)) return GPUOS_SHAPE_MISMATCH;
+  if (in.rank == 0 || in.extents[in.rank - 1] == 0) return GPUOS_EMPTY_AXIS;
+  int b;
+  if ((b = bind_code(in)) || (b = bind_code(out))) return b;
+  const int dt = out.dtype;
+  const int64_t cols = in.extents[in.rank - 1];
+  const int64_t si = in.strides[in.rank - 1], so = out.strides[out.rank - 1];
+  RowIter it;
+  it.init(in);
+  RowSched rs;
+  rs.init(c, it.rows, cols);
+  char* scratch = c->smem;
+  // whole-group units visit identical rows, so their barriers stay matched
+  for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
+    int64_t oi, oo;
+    it.offsets(row, in.strides, out.strides, &oi, &oo);
+    const char* ib = (const char*)in.addr + oi * dtype_width(dt);
+    char* ob = (char*)out.addr + oo * dtype_width(dt);
+    const double mx = row_max_scan(dt, ib, si, cols, rs, c, scratch);
+    double s = 0.0;
+    for (int64_t j = rs.lane; j < cols; j += rs.width) s += exp(__dsub_rn(load_any(dt, ib, j * si), mx));
+    const double denom = unit_sum(s, rs, c, (double*)scratch);
+    for (int64_t j = rs.lane; j < cols; j += rs.width) {
+      const double e = exp(__dsub_rn(load_any(dt, ib, j * si), mx));
+      store_any(dt, ob, j * so, __ddiv_rn(e, denom));
+    }
+  }
+  return GPUOS_OK;
+}
+
+// ---- layernorm: inputs {x, gamma, beta}, scalars[0] = eps ----
+__device__ __noinline__ int op_layernorm(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 3) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& in = t->views[1];
+  const gpuos_view& g = t->views[2];
+  const gpuos_view& be = t->views[3];
+  if (!is_float_dt(out.dtype)) return GPUOS_DTYPE_MISMATCH;
+  if (in.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (!same_shape(in, out)) return GPUOS_SHAPE_MISMATCH;
+  if (in.rank == 0 || in.extents[in.rank - 1] == 0) return GPUOS_EMPTY_AXIS;
+  if (g.dtype != out.dtype || be.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  const double eps = t->n_scalars == 0 ? 1e-5 : t->scalars[0];
+  const int64_t cols = in.extents[in.rank - 1];
+  // broadcast_view(gamma, {cols}) / (beta, {cols})
+  int64_t gs, bs;
+  {
+    if (g.rank > 1 || be.rank > 1) return GPUOS_INCOMPATIBLE_SHAPES;
+    if (g.rank == 1 && g.extents[0] != cols && g.extents[0] != 1) return GPUOS_INCOMPATIBLE_SHAPES;
+    gs = (g.rank == 1 && g.extents[0] == cols) ? g.strides[0] : 0;
+    if (be.rank == 1 && be.extents[0] != cols && be.extents[0] != 1) return GPUOS_INCOMPATIBLE_SHAPES;
+    bs = (be.rank == 1 && be.extents[0] == cols) ? be.strides[0] : 0;
+  }
+  int b;
+  if ((b = bind_code(in)) || (b = bind_code(out)) || (b = bind_code(g)) || (b = bind_code(be))) return b;
+  const int dt = out.dtype;
+  const int64_t si = in.strides[in.rank - 1], so = out.strides[out.rank - 1];
+  RowIter it;
+  it.init(in);
+  RowSched rs;
+  rs.init(c, it.rows, cols);
+  double* red = (double*)c->smem;
+  const double dcols = (double)cols;
+  for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
+    int64_t oi, oo;
+    it.offsets(row, in.strides, out.strides, &oi, &oo);
+    const char* ib = (const char*)in.addr + oi * dtype_width(dt);
+    char* ob = (char*)out.addr + oo * dtype_width(dt);
+    double s = 0.0;
+    for (int64_t j = rs.lane; j < cols; j += rs.width) s += load_any(dt, ib, j * si);
+    const double mean = __ddiv_rn(unit_sum(s, rs, c, red), dcols);
+    double v = 0.0;
+    for (int64_t j = rs.lane; j < cols; j += rs.width) {
+      const double d = __dsub_rn(load_any(dt, ib, j * si), mean);
+      v = __dadd_rn(v, __dmul_rn(d, d));
+    }
+    const double var = __ddiv_rn(unit_sum(v, rs, c, red), dcols);
+    const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, eps)));
+    for (int64_t j = rs.lane; j < cols; j += rs.width) {
+      const double xhat = __dmul_rn(__dsub_rn(load_any(dt, ib, j * si), mean), inv);
+      const double gv = load_any(dt, (const char*)g.addr, j * gs);
+      const double bv = load_any(dt, (const char*)be.addr, j * bs);
+      store_any(dt, ob, j * so, __dadd_rn(__dmul_rn(xhat, gv), bv));
+    }
+  }
+  return GPUOS_OK;
+}
+
+// ---- reductions over the last axis ----
+template <int MODE>  // 0 sum, 1 max, 2 min
+__device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
+  if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& in = t->views[1];
+  if (in.dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+  if (in.rank == 0) return GPUOS_EMPTY_AXIS;
+  if (out.rank != in.rank - 1) return GPUOS_SHAPE_MISMATCH;
+  for (int d = 0; d < out.rank; ++d)
+    if (out.extents[d] != in.extents[d]) return GPUOS_SHAPE_MISMATCH;
+  const int64_t cols = in.extents[in.rank - 1];
+  if (cols == 0 && MODE != 0) return GPUOS_EMPTY_AXIS;
+  int b;
+  if ((b = bind_code(in)) || (b = bind_code(out))) return b;
+  const int dt = out.dtype;
+  const int64_t si = in.strides[in.rank - 1];
+  RowIter it;
+  it.init(in);
+  RowSched rs;
+  rs.init(c, it.rows, cols);
+  for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
+    int64_t oi, oo;
+    it.offsets(row, in.strides, out.strides, &oi, &oo);
+    const char* ib = (const char*)in.addr + oi * dtype_width(dt);
+    char* ob = (char*)out.addr + oo * dtype_width(dt);
+    double r;
+    if (MODE == 0) {
+      if (dt == GPUOS_I32) {
+        // exact integer accumulation == the reference's exact-in-double sum
+        long long s = 0;
+        for (int64_t j = rs.lane; j < cols; j += rs.width) s += ((const int32_t*)ib)[j * si];
+        r = (double)(long long)unit_sum((double)s, rs, c, (double*)c->smem);
+      } else {
+        double s = 0.0;
+        for (int64_t j = rs.lane; j < cols; j += rs.width) s += load_any(dt, ib, j * si);
+        r = unit_sum(s, rs, c, (double*)c->smem);
+      }
+    } else {
+      Ext e;
+      e.v = 0.0;
+      e.i = -1;
+      for (int64_t j = rs.lane; j < cols; j += rs.width) {
+        const double x = load_any(dt, ib, j * si);
+        if (x == x) {
+          Ext y;
+          y.v = x;
+          y.i = j;
+          e = ext_merge(e, y, MODE == 1);
+        }
+      }
+      e = unit_ext(e, MODE == 1, rs, c, c->smem);
+      const double x0 = load_any(dt, ib, 0);
+      r = (x0 != x0 || e.i < 0) ? x0 : e.v;
+    }
+    if (rs.lane == 0) store_any(dt, ob, 0, r);
+  }
+  return GPUOS_OK;
+}
+
+__device__ __noinline__ int op_reduce_sum(const gpuos_task* t, const Ctx* c) { return reduce_body<0>(t, c); }
+__device__ __noinline__ int op_reduce_max(const gpuos_task* t, const Ctx* c) { return reduce_body<1>(t, c); }
+__device__ __noinline__ int op_reduce_min(const gpuos_task* t, const Ctx* c) { return reduce_body<2>(t, c); }
+
+}  // namespace gdev
