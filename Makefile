@@ -1,0 +1,52 @@
+# Build recipe for the B200 GPUOS runtime.  Everything is compiled for sm_100a
+# with nvcc (device code) or g++ (host code over the C-ABI).  `make` builds:
+#   paper_2604_17861_b200/lib/libgpuos_cuda.so   device runtime + C-ABI
+#   paper_2604_17861_b200/lib/libgpuos_bench.so  bench driver (bench.py)
+#   build/cpp/test_runtime                       C++ runtime parity suite
+#   oracle/liboracle.so                          CPU restatement (tests only)
+#   oracle/_ref/*                                 reference built from /root/reference (when present)
+NVCC ?= nvcc
+CXX ?= g++
+CC ?= gcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
+CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -Iinclude -Ipaper_2604_17861_b200/include
+LIBDIR := paper_2604_17861_b200/lib
+CSRC := paper_2604_17861_b200/csrc
+OBJ := build/obj
+DEV_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dev_state.h include/gpuos_cuda.h
+HOST_HDRS := $(wildcard paper_2604_17861_b200/include/gpuos/*.hpp) include/gpuos_cuda.h
+
+all: lib bench cpp-tests oracle
+
+lib: $(LIBDIR)/libgpuos_cuda.so
+bench: $(LIBDIR)/libgpuos_bench.so
+cpp-tests: build/cpp/test_runtime
+
+$(OBJ)/worker.o: $(CSRC)/worker.cu $(DEV_HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -Xptxas -dlcm=cg -c $< -o $@
+
+$(OBJ)/capi.o: $(CSRC)/capi.cu $(DEV_HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/libgpuos_cuda.so: $(OBJ)/worker.o $(OBJ)/capi.o
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lnvrtc -lnvJitLink
+
+$(LIBDIR)/libgpuos_bench.so: tools/bench/gpuos_bench.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN'
+
+build/cpp/test_runtime: tests/cpp/test_runtime.cpp tests/cpp/check.hpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	@mkdir -p build/cpp
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIBDIR)/*.so
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib bench cpp-tests oracle clean

@@ -1,0 +1,290 @@
+#!/usr/bin/env python3
+"""Benchmark: small-op tasks/s through the persistent B200 GPUOS runtime.
+
+Workload (BASELINE.json metric, configs[0]/[1] headline): one step = 10,000
+fp32 Add tasks of 4,096 contiguous elements on one task ring with the builtin
+table, distinct a_i/b_i/c_i per task (491.5 MB working set, > 126 MB L2),
+submitted through gpuos::Runtime::submit.  A step launches the persistent
+worker kernel, submits every task, waits, and retires the kernel with the
+shutdown sentinel; its duration is measured with CUDA events bracketing the
+worker kernel on its own stream.  ``value`` = tasks of all ranks / max-over-
+ranks time.  Also reported: baseline (a) one cudaLaunchKernel per task, queue-
+depth-1 submit->complete latency, the e2e arm (inputs and outputs in pinned
+host memory, copies in the timed region), the roofline of the worker kernel,
+the reference CPU implementation (oracle/_ref) timed on the host cores, and
+SM clocks sampled during the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+LIBDIR = os.path.join(ROOT, "paper_2604_17861_b200", "lib")
+METRIC = "small-op tasks/sec and p50 submit-to-complete µs (4K-elem fp32 ops), 1-8 B200"
+N_TASKS, N_ELEMS = 10_000, 4096
+BYTES_PER_TASK = N_ELEMS * 12  # 2 x 16 KiB read + 16 KiB write
+WORKLOAD = ("config1: 10,000 fp32 Add tasks x 4096 contiguous elements per step, one task ring, "
+            "builtin op table, distinct buffers per task")
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus: int):
+    if n_gpus <= 1 or "RANK" not in os.environ:
+        return None, 0, 1, 0
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend="gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return dist, rank, world, local
+
+
+def dist_max(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def ref_cpu_baseline(seconds: float, steps: int = 0) -> dict | None:
+    """The reference gpuos::Runtime (built from /root/reference into oracle/_ref)
+    on the host cores: config-1 steps of 10,000 add tasks, all host threads."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    cmd = [exe, "--tasks", str(N_TASKS), "--elems", str(N_ELEMS), "--seconds", str(seconds)]
+    if steps:
+        cmd += ["--steps", str(steps)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    for line in out.stdout.splitlines():
+        if line.startswith("{"):
+            return json.loads(line)
+    return None
+
+
+def run_reference(args) -> None:
+    dist, rank, world, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    res = ref_cpu_baseline(seconds=0, steps=args.steps + args.warmup)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
+        return
+    timed = res["step_seconds"][args.warmup:]
+    tot = sum(timed)
+    value = N_TASKS * len(timed) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tasks/s", "n_gpus": args.gpus,
+        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "tasks_per_step": N_TASKS, "elems": N_ELEMS,
+                   "parallelism": "host threads (reference worker pool)"},
+        "cpu_baseline": {"value": value, "unit": "tasks/s", "cores": res["workers"], "kind": "reference",
+                         "sample": f"{len(timed)} steps x {N_TASKS} tasks x {N_ELEMS} fp32 adds"},
+        "e2e": {"value": value, "unit": "tasks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "p50_submit_to_complete_us": res.get("p50_us"),
+    }
+    print(json.dumps(line))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workers", type=int, default=0)
+    ap.add_argument("--capacity", type=int, default=4096)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    dist, rank, world, local = dist_setup(args.gpus)
+    lib_path = os.path.join(LIBDIR, "libgpuos_bench.so")
+    if not os.path.exists(lib_path):
+        raise SystemExit("libgpuos_bench.so not built: run __graft_entry__.build()")
+    lib = C.CDLL(lib_path)
+    lib.gb_open.restype = C.c_void_p
+    lib.gb_open.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.gb_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_latency.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_verify.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]
+    lib.gb_info.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+    lib.gb_close.argtypes = [C.c_void_p]
+
+    h = lib.gb_open(local, N_TASKS, N_ELEMS, args.workers, args.capacity)
+    out = (C.c_double * 8)()
+
+    def step(mode):
+        rc = lib.gb_step(h, mode, out)
+        assert rc == 0
+        return out[0], out[1], out[4], out[5]
+
+    for _ in range(args.warmup):
+        step(0)
+    dist_barrier(dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    dev_ms, host_ms, sub_ms, fallbacks = [], [], [], 0
+    for _ in range(args.steps):
+        d, hm, fb, sm = step(0)
+        dev_ms.append(d)
+        host_ms.append(hm)
+        sub_ms.append(sm)
+        fallbacks += int(fb)
+    clk = clocks.stop()
+    dist_barrier(dist)
+    total_dev_s = dist_max(dist, sum(dev_ms) / 1e3)
+    total_host_s = dist_max(dist, sum(host_ms) / 1e3)
+    bad, checked = C.c_uint64(), C.c_uint64()
+    lib.gb_verify(h, C.byref(bad), C.byref(checked), 0)
+
+    # baseline (a): one cudaLaunchKernel per task, same bodies
+    base_steps = max(1, min(args.steps, 3))
+    step(1)  # warm
+    b_dev = [step(1)[0] for _ in range(base_steps)]
+    # queue-depth-1 latency, persistent vs per-op launch
+    lat = (C.c_double * 3)()
+    lib.gb_latency(h, 0, 10_000, 1_000, lat)
+    p50, p99 = lat[0], lat[1]
+    lib.gb_latency(h, 1, 2_000, 200, lat)
+    lp50, lp99 = lat[0], lat[1]
+    # e2e arm: host buffers, copies inside the timed region
+    step(2)
+    e2e_ms = [step(2)[1] for _ in range(max(1, min(args.steps, 5)))]
+    e_bad, e_checked = C.c_uint64(), C.c_uint64()
+    lib.gb_verify(h, C.byref(e_bad), C.byref(e_checked), 1)
+    info = C.create_string_buffer(512)
+    lib.gb_info(h, info, 512)
+    lib.gb_close(h)
+
+    if rank != 0:
+        dist_barrier(dist)
+        return
+    tasks_total = N_TASKS * args.steps * world
+    value = tasks_total / total_dev_s
+    per_step_dev_ms = 1e3 * total_dev_s / args.steps
+    peaks = load_peaks()
+    achieved_gbs = (N_TASKS * BYTES_PER_TASK) / (per_step_dev_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "worker_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("bytes_per_step")
+    base_value = N_TASKS / (statistics.median(b_dev) / 1e3)
+    e2e_value = N_TASKS / (statistics.median(e2e_ms) / 1e3)
+    cpu = None
+    if not args.no_cpu_baseline:
+        r = ref_cpu_baseline(seconds=args.cpu_seconds)
+        if r is not None:
+            cpu = {"value": r["tasks_per_s"], "unit": "tasks/s", "cores": r["workers"], "kind": "reference",
+                   "sample": f"{r['tasks']} config-1 add tasks x {N_ELEMS} fp32 ({r['seconds']:.1f} s)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tasks/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step_dev_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "tasks_per_step": N_TASKS, "elems": N_ELEMS, "global_batch": N_TASKS * world,
+                   "l2": "inputs larger than L2 (491.5 MB distinct buffers per step)",
+                   "parallelism": f"independent ring + persistent kernel per GPU x{world}",
+                   "runtime": json.loads(info.value.decode())},
+        "p50_submit_to_complete_us": p50, "p99_submit_to_complete_us": p99,
+        "host_clock_tasks_per_s": tasks_total / total_host_s,
+        "host_submit_ns_per_task": 1e6 * statistics.median(sub_ms) / N_TASKS,
+        "baseline_per_op_launch": {"value": base_value, "unit": "tasks/s", "p50_launch_sync_us": lp50,
+                                   "p99_launch_sync_us": lp99, "speedup": value / base_value},
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
+                     "kernel": "gpuos_worker_kernel (per step: 10,000 x 49,152 algorithmic bytes)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "tasks/s", "h2d_bytes_per_step": 2 * N_TASKS * N_ELEMS * 4,
+                "d2h_bytes_per_step": N_TASKS * N_ELEMS * 4},
+        "gpu_launches": args.steps,
+        "parity": {"mismatches": bad.value, "checked": checked.value, "e2e_mismatches": e_bad.value},
+        "queue_full_fallbacks": fallbacks,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    dist_barrier(dist)
+
+
+if __name__ == "__main__":
+    main()

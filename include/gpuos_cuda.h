@@ -229,6 +229,9 @@ int gpuos_dev_stop(gpuos_dev* dev);
 int gpuos_dev_start(gpuos_dev* dev);
 int gpuos_dev_num_workers(gpuos_dev* dev, uint32_t* n);
 int gpuos_dev_sm_count(gpuos_dev* dev, uint32_t* n);
+/* Hold (1) / release (0) ticket claims: idle workers stop claiming while held,
+ * so published work stays queued (lets tests fill the ring; stop releases). */
+int gpuos_dev_hold(gpuos_dev* dev, int hold);
 /* Live yield cadence (executor.hpp:107). */
 int gpuos_set_yield_every(gpuos_dev* dev, uint64_t n);
 /* Convert a device %globaltimer stamp to host steady_clock ns. */
@@ -263,6 +266,8 @@ int gpuos_ring_publish(gpuos_dev* dev, uint64_t pos, const gpuos_task* task);
 int gpuos_ring_peek(gpuos_dev* dev, gpuos_snapshot* out);
 /* Block until processed >= `count` (wait_all, runtime.hpp:399-406). */
 int gpuos_ring_wait_processed(gpuos_dev* dev, uint64_t count);
+/* One-line JSON of the ring cursors and device control words (diagnostics). */
+int gpuos_dev_debug(gpuos_dev* dev, char* buf, size_t cap);
 
 /* ---------------- operator table (OperatorTable, optable.hpp:98-251) ---------------- */
 int gpuos_table_slots(gpuos_dev* dev, uint32_t* slots);
@@ -283,6 +288,22 @@ int gpuos_trace_enable(gpuos_dev* dev, int on);
 /* Copy up to `cap` most recent device tracepoints (oldest first), host clock. */
 int gpuos_trace_snapshot(gpuos_dev* dev, gpuos_tracepoint* out, uint64_t cap, uint64_t* n);
 
+/* Per-task phase stamps of the same records, all on the host steady clock:
+ * commit, ticket taken by the claiming worker, publication observed, table
+ * resolved (dequeue), body finished, completion posted. */
+typedef struct gpuos_trace_phase {
+  uint64_t seq;
+  uint64_t enqueue_ns;
+  uint64_t ticket_ns;
+  uint64_t seen_ns;
+  uint64_t dequeue_ns;
+  uint64_t end_ns;
+  uint64_t done_ns;
+  uint32_t worker;
+  uint32_t reserved;
+} gpuos_trace_phase;
+int gpuos_trace_phases(gpuos_dev* dev, gpuos_trace_phase* out, uint64_t cap, uint64_t* n);
+
 /* ---------------- conventional path / baseline (a) ---------------- */
 /* One cudaLaunchKernel of the same task body as a standalone kernel
  * (execute_inline, runtime.hpp:567-619).  `stream` is a cudaStream_t or NULL
@@ -291,6 +312,21 @@ int gpuos_launch_task(gpuos_dev* dev, const gpuos_task* task, void* stream);
 int gpuos_stream_create(gpuos_dev* dev, void** stream);
 int gpuos_stream_sync(gpuos_dev* dev, void* stream);
 int gpuos_stream_destroy(gpuos_dev* dev, void* stream);
+
+/* ---------------- timing and host staging (bench / e2e) ---------------- */
+/* The stream the persistent worker kernel is launched on.  An event recorded
+ * there before gpuos_dev_start and another after it completes when the
+ * worker kernel exits, so a pair brackets one kernel lifetime. */
+int gpuos_dev_kernel_stream(gpuos_dev* dev, void** stream);
+int gpuos_event_create(gpuos_dev* dev, void** event);
+int gpuos_event_record(gpuos_dev* dev, void* event, void* stream);
+int gpuos_event_sync(gpuos_dev* dev, void* event);
+int gpuos_event_elapsed_ms(gpuos_dev* dev, void* start, void* stop, float* ms);
+int gpuos_event_destroy(gpuos_dev* dev, void* event);
+/* Pinned host staging memory (freed at gpuos_dev_close). */
+int gpuos_host_alloc(gpuos_dev* dev, uint64_t bytes, void** ptr);
+/* dir as gpuos_buf_copy; enqueued on `stream` (NULL = side stream), not synchronised. */
+int gpuos_copy_async(gpuos_dev* dev, void* dst, const void* src, uint64_t bytes, int dir, void* stream);
 
 /* ---------------- NVRTC / nvJitLink (ModuleCache compile step, opcompiler.hpp:180-189) ---------------- */
 /* Compile CUDA source to a relocatable sm_100a cubin and link it with nvJitLink.

@@ -77,6 +77,12 @@ class Tracepoint(C.Structure):
                 ("exec_ns", C.c_uint64), ("version", C.c_uint64)]
 
 
+class TracePhase(C.Structure):
+    _fields_ = [("seq", C.c_uint64), ("enqueue_ns", C.c_uint64), ("ticket_ns", C.c_uint64),
+                ("seen_ns", C.c_uint64), ("dequeue_ns", C.c_uint64), ("end_ns", C.c_uint64),
+                ("done_ns", C.c_uint64), ("worker", C.c_uint32), ("reserved", C.c_uint32)]
+
+
 class Instr(C.Structure):
     _fields_ = [("op", C.c_uint8), ("pad", C.c_uint8 * 3), ("k", C.c_int32), ("value", C.c_double)]
 
@@ -92,13 +98,15 @@ assert C.sizeof(View) == 48 and C.sizeof(Task) == SLOT_BYTES and C.sizeof(Instr)
 EXPORTS = [
     "gpuos_abi_version", "gpuos_default_cfg", "gpuos_dev_open", "gpuos_dev_close", "gpuos_dev_alive",
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
-    "gpuos_set_yield_every", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
+    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
     "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
-    "gpuos_ring_wait_processed", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
+    "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
     "gpuos_table_install_builtin", "gpuos_table_install_program", "gpuos_table_kill",
-    "gpuos_dev_get_stats", "gpuos_trace_enable", "gpuos_trace_snapshot", "gpuos_launch_task",
-    "gpuos_stream_create", "gpuos_stream_sync", "gpuos_stream_destroy", "gpuos_jit_compile", "gpuos_free",
+    "gpuos_dev_get_stats", "gpuos_trace_enable", "gpuos_trace_snapshot", "gpuos_trace_phases", "gpuos_launch_task",
+    "gpuos_stream_create", "gpuos_stream_sync", "gpuos_stream_destroy", "gpuos_dev_kernel_stream",
+    "gpuos_event_create", "gpuos_event_record", "gpuos_event_sync", "gpuos_event_elapsed_ms",
+    "gpuos_event_destroy", "gpuos_host_alloc", "gpuos_copy_async", "gpuos_jit_compile", "gpuos_free",
     "gpuos_error_name",
 ]
 
@@ -125,6 +133,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_dev_num_workers": ([P, C.POINTER(U32)], I),
         "gpuos_dev_sm_count": ([P, C.POINTER(U32)], I),
         "gpuos_set_yield_every": ([P, U64], I),
+        "gpuos_dev_hold": ([P, I], I),
         "gpuos_dev_clock_offset": ([P, C.POINTER(C.c_int64)], I),
         "gpuos_buf_alloc": ([P, I, U64, C.POINTER(U64), C.POINTER(P)], I),
         "gpuos_buf_free": ([P, U64], I),
@@ -139,6 +148,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_ring_publish": ([P, U64, C.POINTER(Task)], I),
         "gpuos_ring_peek": ([P, C.POINTER(Snapshot)], I),
         "gpuos_ring_wait_processed": ([P, U64], I),
+        "gpuos_dev_debug": ([P, C.c_char_p, C.c_size_t], I),
         "gpuos_table_slots": ([P, C.POINTER(U32)], I),
         "gpuos_table_version": ([P, C.POINTER(U64)], I),
         "gpuos_table_status": ([P, U32, C.POINTER(I), C.POINTER(I)], I),
@@ -148,10 +158,19 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_dev_get_stats": ([P, C.POINTER(DevStats)], I),
         "gpuos_trace_enable": ([P, I], I),
         "gpuos_trace_snapshot": ([P, C.POINTER(Tracepoint), U64, C.POINTER(U64)], I),
+        "gpuos_trace_phases": ([P, C.POINTER(TracePhase), U64, C.POINTER(U64)], I),
         "gpuos_launch_task": ([P, C.POINTER(Task), P], I),
         "gpuos_stream_create": ([P, C.POINTER(P)], I),
         "gpuos_stream_sync": ([P, P], I),
         "gpuos_stream_destroy": ([P, P], I),
+        "gpuos_dev_kernel_stream": ([P, C.POINTER(P)], I),
+        "gpuos_event_create": ([P, C.POINTER(P)], I),
+        "gpuos_event_record": ([P, P, P], I),
+        "gpuos_event_sync": ([P, P], I),
+        "gpuos_event_elapsed_ms": ([P, P, P, C.POINTER(C.c_float)], I),
+        "gpuos_event_destroy": ([P, P], I),
+        "gpuos_host_alloc": ([P, U64, C.POINTER(P)], I),
+        "gpuos_copy_async": ([P, P, P, U64, I, P], I),
         "gpuos_jit_compile": ([C.c_char_p, C.POINTER(C.c_char_p), I, C.POINTER(P), C.POINTER(C.c_size_t),
                                C.POINTER(U64), C.POINTER(U64), C.c_char_p, C.c_size_t], I),
         "gpuos_free": ([P], None),
@@ -241,6 +260,9 @@ class Device:
     def start(self) -> int:
         return self.lib.gpuos_dev_start(self.h)
 
+    def hold(self, on: bool) -> None:
+        _ck(self.lib.gpuos_dev_hold(self.h, int(on)), "hold")
+
     # -- buffers / views --
     def alloc(self, dtype: int, n: int) -> Buffer:
         bid, ptr = C.c_uint64(), C.c_void_p()
@@ -312,7 +334,7 @@ class Device:
             if w & 0xFF:
                 return (w >> 8) & 0xFF
             if time.time() - t0 > timeout:
-                raise TimeoutError(f"task seq={t.seq} op={t.op_id} not completed")
+                raise TimeoutError(f"task seq={t.seq} op={t.op_id} not completed: {self.debug()}")
 
     def run(self, op_id: int, out: View, inputs: Sequence[View] = (), scalars: Sequence[float] = (),
             flags: int = 0) -> int:
@@ -335,6 +357,11 @@ class Device:
 
     def wait_processed(self, count: int) -> None:
         _ck(self.lib.gpuos_ring_wait_processed(self.h, count), "wait_processed")
+
+    def debug(self) -> str:
+        buf = C.create_string_buffer(4096)
+        self.lib.gpuos_dev_debug(self.h, buf, 4096)
+        return buf.value.decode()
 
     def peek(self) -> Snapshot:
         s = Snapshot()
@@ -372,6 +399,12 @@ class Device:
         s = DevStats()
         _ck(self.lib.gpuos_dev_get_stats(self.h, C.byref(s)), "stats")
         return s
+
+    def phases(self, cap: int = 65536):
+        arr = (TracePhase * cap)()
+        n = C.c_uint64()
+        _ck(self.lib.gpuos_trace_phases(self.h, arr, cap, C.byref(n)), "phases")
+        return [arr[i] for i in range(n.value)]
 
     def trace(self, cap: int = 65536):
         arr = (Tracepoint * cap)()

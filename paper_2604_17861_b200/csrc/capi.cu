@@ -113,6 +113,38 @@ struct gpuos_dev {
     }                                                           \
   } while (0)
 
+// Process-wide bookkeeping: cudaFree / cudaFreeHost block while any worker
+// kernel of the same context is resident, so a runtime closing while another
+// one is running parks its allocations here; the last runtime of a device to
+// stop frees them.
+namespace {
+struct Grave {
+  std::vector<void*> dev, managed, pinned;
+};
+std::mutex g_life_mu;
+std::unordered_map<int, int> g_resident;
+std::unordered_map<int, Grave> g_grave;
+
+void note_resident(int device, int delta) {
+  std::lock_guard<std::mutex> lk(g_life_mu);
+  g_resident[device] += delta;
+}
+
+void bury_and_maybe_free(int device, Grave&& g) {
+  std::lock_guard<std::mutex> lk(g_life_mu);
+  Grave& all = g_grave[device];
+  all.dev.insert(all.dev.end(), g.dev.begin(), g.dev.end());
+  all.managed.insert(all.managed.end(), g.managed.begin(), g.managed.end());
+  all.pinned.insert(all.pinned.end(), g.pinned.begin(), g.pinned.end());
+  if (g_resident[device] > 0) return;
+  cudaSetDevice(device);
+  for (void* p : all.dev) cudaFree(p);
+  for (void* p : all.managed) cudaFree(p);
+  for (void* p : all.pinned) cudaFreeHost(p);
+  all = Grave{};
+}
+}  // namespace
+
 static BufRec* buf_rec(gpuos_dev* d, uint64_t id) {
   const uint64_t c = id >> kBufChunkBits;
   if (id == 0 || c >= d->buf_chunks.size()) return nullptr;
@@ -172,13 +204,14 @@ static int calibrate_clocks(gpuos_dev* d) {
     GPUOS_CK(cudaStreamSynchronize(d->side));
     const uint64_t h1 = steady_ns();
     uint64_t gt = 0;
-    GPUOS_CK(cudaMemcpy(&gt, dbuf, 8, cudaMemcpyDeviceToHost));
+    GPUOS_CK(cudaMemcpyAsync(&gt, dbuf, 8, cudaMemcpyDeviceToHost, d->side));
+    GPUOS_CK(cudaStreamSynchronize(d->side));
     if ((int64_t)(h1 - h0) < best_rtt) {
       best_rtt = (int64_t)(h1 - h0);
       d->gt_offset = (int64_t)((h0 + h1) / 2) - (int64_t)gt;
     }
   }
-  GPUOS_CK(cudaFree(dbuf));
+  d->dev_blocks.push_back(dbuf);  // freed at close (cudaFree blocks behind resident kernels)
   // TSC rate for cheap enqueue stamps
   d->tsc0 = __rdtsc();
   d->ns0 = steady_ns();
@@ -194,6 +227,7 @@ static uint64_t tsc_to_ns(const gpuos_dev* d, uint64_t tsc) {
 
 static int launch_workers(gpuos_dev* d) {
   GPUOS_CK(gdev::launch_worker(d->S, d->workers, d->threads, d->smem, d->ks));
+  note_resident(d->device, +1);
   d->running.store(true, std::memory_order_release);
   return GPUOS_OK;
 }
@@ -265,17 +299,17 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   GPUOS_CK(cudaMalloc(&d->S, sizeof(DevState)));
   GPUOS_CK(cudaMalloc(&d->dbank[0], cfg.table_slots * sizeof(TableEntry)));
   GPUOS_CK(cudaMalloc(&d->dbank[1], cfg.table_slots * sizeof(TableEntry)));
-  GPUOS_CK(cudaMemset(d->dbank[0], 0, cfg.table_slots * sizeof(TableEntry)));
-  GPUOS_CK(cudaMemset(d->dbank[1], 0, cfg.table_slots * sizeof(TableEntry)));
+  GPUOS_CK(cudaMemsetAsync(d->dbank[0], 0, cfg.table_slots * sizeof(TableEntry), d->side));
+  GPUOS_CK(cudaMemsetAsync(d->dbank[1], 0, cfg.table_slots * sizeof(TableEntry), d->side));
   d->bank[0].assign(cfg.table_slots, TableEntry{});
   d->bank[1].assign(cfg.table_slots, TableEntry{});
   GPUOS_CK(cudaMalloc(&d->dev_epoch, W * 8));
-  GPUOS_CK(cudaMemset(d->dev_epoch, 0xff, W * 8));
+  GPUOS_CK(cudaMemsetAsync(d->dev_epoch, 0xff, W * 8, d->side));
   d->trace_cap = cfg.trace_capacity;
   GPUOS_CK(cudaMalloc(&d->dtrace, d->trace_cap * sizeof(gdev::TraceRec)));
-  GPUOS_CK(cudaMemset(d->dtrace, 0, d->trace_cap * sizeof(gdev::TraceRec)));
+  GPUOS_CK(cudaMemsetAsync(d->dtrace, 0, d->trace_cap * sizeof(gdev::TraceRec), d->side));
   GPUOS_CK(cudaMalloc(&d->launch_counters, gdev::kLaunchCounters * 4));
-  GPUOS_CK(cudaMemset(d->launch_counters, 0, gdev::kLaunchCounters * 4));
+  GPUOS_CK(cudaMemsetAsync(d->launch_counters, 0, gdev::kLaunchCounters * 4, d->side));
 
   DevState& s = d->shadow;
   std::memset(&s, 0, sizeof(s));
@@ -304,11 +338,11 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   s.dev_epoch = d->dev_epoch;
   s.trace = d->dtrace;
   s.trace_cap = d->trace_cap;
-  GPUOS_CK(cudaMemcpy(d->S, &s, sizeof(s), cudaMemcpyHostToDevice));
+  GPUOS_CK(cudaMemcpyAsync(d->S, &s, sizeof(s), cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
 
   int rc = calibrate_clocks(d.get());
   if (rc) return rc;
-  GPUOS_CK(cudaDeviceSynchronize());
   rc = launch_workers(d.get());
   if (rc) return rc;
   *out = d.release();
@@ -320,6 +354,7 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
 int gpuos_dev_stop(gpuos_dev* d) {
   if (!d) return GPUOS_INTERNAL;
   if (!d->running.load(std::memory_order_acquire)) return GPUOS_OK;
+  if (d->shadow.hold) gpuos_dev_hold(d, 0);  // held workers could not drain
   uint64_t pos = 0;
   for (;;) {
     if (gpuos_ring_reserve(d, &pos) == GPUOS_OK) break;
@@ -333,6 +368,7 @@ int gpuos_dev_stop(gpuos_dev* d) {
   GPUOS_CK(cudaSetDevice(d->device));
   GPUOS_CK(cudaStreamSynchronize(d->ks));
   d->running.store(false, std::memory_order_release);
+  note_resident(d->device, -1);
   return GPUOS_OK;
 }
 
@@ -357,16 +393,13 @@ int gpuos_dev_close(gpuos_dev* d) {
   if (!d) return GPUOS_OK;
   gpuos_dev_stop(d);
   cudaSetDevice(d->device);
-  cudaDeviceSynchronize();
-  cudaFree(d->S);
-  cudaFree(d->dbank[0]);
-  cudaFree(d->dbank[1]);
-  cudaFree(d->dev_epoch);
-  cudaFree(d->dtrace);
-  cudaFree(d->launch_counters);
-  for (void* p : d->dev_blocks) cudaFree(p);
-  for (void* p : d->managed_blocks) cudaFree(p);
-  for (void* p : d->pinned_blocks) cudaFreeHost(p);
+  cudaStreamSynchronize(d->side);
+  Grave g;
+  g.dev = {d->S, d->dbank[0], d->dbank[1], d->dev_epoch, d->dtrace, d->launch_counters};
+  g.dev.insert(g.dev.end(), d->dev_blocks.begin(), d->dev_blocks.end());
+  g.managed = d->managed_blocks;
+  g.pinned = d->pinned_blocks;
+  bury_and_maybe_free(d->device, std::move(g));
   cudaStreamDestroy(d->ks);
   cudaStreamDestroy(d->side);
   delete d;
@@ -396,6 +429,13 @@ int gpuos_set_yield_every(gpuos_dev* d, uint64_t n) {
   cudaSetDevice(d->device);
   d->shadow.yield_every = n;
   return dev_write_field(d, offsetof(DevState, yield_every), &n, 8);
+}
+
+int gpuos_dev_hold(gpuos_dev* d, int hold) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  d->shadow.hold = hold ? 1u : 0u;
+  return dev_write_field(d, offsetof(DevState, hold), &d->shadow.hold, 4);
 }
 
 int gpuos_dev_clock_offset(gpuos_dev* d, int64_t* off) {
@@ -572,7 +612,8 @@ int gpuos_ring_reserve(gpuos_dev* d, uint64_t* pos) {
   if (__atomic_load_n(w, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
   d->reserve = p + 1;
   *pos = p;
-  _mm_prefetch(d->ring + ((p + 8) & d->mask) * GPUOS_SLOT_BYTES, _MM_HINT_T0);
+  // the device freed upcoming slots over PCIe: pull their sequence words in early
+  _mm_prefetch(d->ring + ((p + 16) & d->mask) * GPUOS_SLOT_BYTES, _MM_HINT_T0);
   return GPUOS_OK;
 }
 
@@ -584,13 +625,17 @@ int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
   w[7] = 0;
   w[7] = slot_checksum(w);
   char* dst = d->ring + (pos & d->mask) * GPUOS_SLOT_BYTES;
-  // body with streaming stores, then the publication word after a fence, then the tail
+  // Streaming stores for the whole slot and the tail: these lines were last
+  // touched by the device (slot free, tail polls), so ordinary stores would
+  // each pay a read-for-ownership.  One sfence makes them globally visible;
+  // a reader that catches the slot half-written fails the checksum and
+  // re-reads, and a tail seen early only wakes a poller one read too soon.
   for (int i = 1; i < GPUOS_SLOT_BYTES / 16; ++i)
     _mm_stream_si128((__m128i*)(dst + 16 * i), _mm_load_si128((const __m128i*)((const char*)w + 16 * i)));
+  _mm_stream_si64((long long*)(dst + 8), (long long)w[1]);
+  _mm_stream_si64((long long*)dst, (long long)w[0]);
+  _mm_stream_si64((long long*)d->tail, (long long)(pos + 1));
   _mm_sfence();
-  __atomic_store_n((uint64_t*)(dst + 8), w[1], __ATOMIC_RELAXED);
-  __atomic_store_n((uint64_t*)dst, w[0], __ATOMIC_RELEASE);
-  __atomic_store_n(d->tail, pos + 1, __ATOMIC_RELEASE);
   d->published.store(pos + 1, std::memory_order_relaxed);
   return GPUOS_OK;
 }
@@ -611,18 +656,61 @@ int gpuos_ring_peek(gpuos_dev* d, gpuos_snapshot* s) {
   return GPUOS_OK;
 }
 
+int gpuos_dev_debug(gpuos_dev* d, char* buf, size_t cap) {
+  if (!d || !buf) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  DevState t;
+  std::memset(&t, 0, sizeof(t));
+  cudaMemcpyAsync(&t, d->S, sizeof(DevState), cudaMemcpyDeviceToHost, d->side);
+  cudaStreamSynchronize(d->side);
+  const uint64_t tail = __atomic_load_n(d->tail, __ATOMIC_ACQUIRE);
+  const uint64_t done = sum_mirror(d, d->mir_done), claimed = sum_mirror(d, d->mir_claimed);
+  // slot publication words around the claim window
+  std::string slots;
+  for (uint64_t p = (tail > 4 ? tail - 4 : 0); p < tail + 4; ++p) {
+    const uint64_t w = *(volatile uint64_t*)(d->ring + (p & d->mask) * GPUOS_SLOT_BYTES);
+    slots += std::to_string(p) + ":" + std::to_string(w) + " ";
+  }
+  std::snprintf(buf, cap,
+                "{\"running\": %d, \"alive\": %d, \"reserve\": %llu, \"tail\": %llu, \"claim\": %llu, \"hint\": %llu, "
+                "\"stop_pos\": %llu, \"version\": %llu, \"hold\": %u, \"processed\": %llu, \"mirror_done\": %llu, "
+                "\"mirror_claimed\": %llu, \"torn\": %llu, \"slots\": \"%s\"}",
+                d->running.load() ? 1 : 0, gpuos_dev_alive(d), (unsigned long long)d->reserve,
+                (unsigned long long)tail, (unsigned long long)t.claim, (unsigned long long)t.hint,
+                (unsigned long long)t.stop_pos, (unsigned long long)t.version, t.hold,
+                (unsigned long long)t.processed, (unsigned long long)done, (unsigned long long)claimed,
+                (unsigned long long)t.torn_reads, slots.c_str());
+  return GPUOS_OK;
+}
+
 int gpuos_ring_wait_processed(gpuos_dev* d, uint64_t count) {
   if (!d) return GPUOS_INTERNAL;
   uint32_t spins = 0;
-  while (sum_mirror(d, d->mir_done) < count) {
+  uint64_t last = 0, t_last = steady_ns();
+  while (true) {
+    const uint64_t done = sum_mirror(d, d->mir_done);
+    if (done >= count) break;
     if (!d->running.load(std::memory_order_acquire)) return GPUOS_RUNTIME_STOPPED;
+    if (done != last) {
+      last = done;
+      t_last = steady_ns();
+    }
     if (++spins < 64) {
       _mm_pause();
     } else if (spins < 256) {
       std::this_thread::yield();
     } else {
       std::this_thread::sleep_for(std::chrono::microseconds(20));
-      if ((spins & 1023) == 0 && !gpuos_dev_alive(d)) return GPUOS_INTERNAL;
+      if ((spins & 1023) == 0) {
+        if (!gpuos_dev_alive(d)) return GPUOS_INTERNAL;
+        if (steady_ns() - t_last > 5000000000ull) {  // no progress for 5 s: say why
+          char buf[2048];
+          gpuos_dev_debug(d, buf, sizeof(buf));
+          std::fprintf(stderr, "gpuos: wait_processed(%llu) stalled at %llu: %s\n", (unsigned long long)count,
+                       (unsigned long long)done, buf);
+          t_last = steady_ns();
+        }
+      }
     }
   }
   return GPUOS_OK;
@@ -828,6 +916,36 @@ int gpuos_trace_snapshot(gpuos_dev* d, gpuos_tracepoint* out, uint64_t cap, uint
   return GPUOS_OK;
 }
 
+int gpuos_trace_phases(gpuos_dev* d, gpuos_trace_phase* out, uint64_t cap, uint64_t* n) {
+  if (!d || !n) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  uint64_t head = 0;
+  GPUOS_CK(cudaMemcpyAsync(&head, (char*)d->S + offsetof(DevState, trace_head), 8, cudaMemcpyDeviceToHost, d->side));
+  std::vector<gdev::TraceRec> recs(d->trace_cap);
+  GPUOS_CK(cudaMemcpyAsync(recs.data(), d->dtrace, d->trace_cap * sizeof(gdev::TraceRec), cudaMemcpyDeviceToHost,
+                           d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  const uint64_t have = std::min<uint64_t>(head, d->trace_cap);
+  auto h = [&](uint64_t gt) { return (uint64_t)((int64_t)gt + d->gt_offset); };
+  uint64_t k = 0;
+  for (uint64_t ticket = head - have; ticket < head && k < cap; ++ticket) {
+    const gdev::TraceRec& r = recs[ticket % d->trace_cap];
+    if (r.stamp != ticket * 2 + 2) continue;
+    gpuos_trace_phase& p = out[k++];
+    p.seq = r.seq;
+    p.enqueue_ns = tsc_to_ns(d, r.enqueue_ns);
+    p.ticket_ns = h(r.t_ticket);
+    p.seen_ns = h(r.t_seen);
+    p.dequeue_ns = h(r.dequeue_gt);
+    p.end_ns = h(r.dequeue_gt + r.exec_ns);
+    p.done_ns = h(r.t_done);
+    p.worker = (uint32_t)r.worker;
+    p.reserved = (uint32_t)(r.pad > r.t_seen ? r.pad - r.t_seen : 0);  // seen -> fenced ns
+  }
+  *n = k;
+  return GPUOS_OK;
+}
+
 // ---------------------------------------------------------------- conventional path
 
 static uint32_t parts_for(const gpuos_dev* d, const gpuos_task* t, uint32_t kind) {
@@ -899,6 +1017,72 @@ int gpuos_stream_destroy(gpuos_dev* d, void* stream) {
   if (!d || !stream) return GPUOS_INTERNAL;
   cudaSetDevice(d->device);
   GPUOS_CK(cudaStreamDestroy((cudaStream_t)stream));
+  return GPUOS_OK;
+}
+
+// ---------------------------------------------------------------- timing / staging
+
+int gpuos_dev_kernel_stream(gpuos_dev* d, void** stream) {
+  if (!d || !stream) return GPUOS_INTERNAL;
+  *stream = (void*)d->ks;
+  return GPUOS_OK;
+}
+
+int gpuos_event_create(gpuos_dev* d, void** ev) {
+  if (!d || !ev) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  cudaEvent_t e;
+  GPUOS_CK(cudaEventCreate(&e));
+  *ev = (void*)e;
+  return GPUOS_OK;
+}
+
+int gpuos_event_record(gpuos_dev* d, void* ev, void* stream) {
+  if (!d || !ev) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaEventRecord((cudaEvent_t)ev, stream ? (cudaStream_t)stream : d->side));
+  return GPUOS_OK;
+}
+
+int gpuos_event_sync(gpuos_dev* d, void* ev) {
+  if (!d || !ev) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaEventSynchronize((cudaEvent_t)ev));
+  return GPUOS_OK;
+}
+
+int gpuos_event_elapsed_ms(gpuos_dev* d, void* a, void* b, float* ms) {
+  if (!d || !a || !b || !ms) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+  return GPUOS_OK;
+}
+
+int gpuos_event_destroy(gpuos_dev* d, void* ev) {
+  if (!d || !ev) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaEventDestroy((cudaEvent_t)ev));
+  return GPUOS_OK;
+}
+
+int gpuos_host_alloc(gpuos_dev* d, uint64_t bytes, void** ptr) {
+  if (!d || !ptr) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  void* p = nullptr;
+  GPUOS_CK(cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable));
+  {
+    std::lock_guard<std::mutex> lk(d->buf_mu);
+    d->pinned_blocks.push_back(p);
+  }
+  *ptr = p;
+  return GPUOS_OK;
+}
+
+int gpuos_copy_async(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int dir, void* stream) {
+  if (!d) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  const cudaMemcpyKind k = dir == 0 ? cudaMemcpyHostToDevice : dir == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  GPUOS_CK(cudaMemcpyAsync(dst, src, bytes, k, stream ? (cudaStream_t)stream : d->side));
   return GPUOS_OK;
 }
 

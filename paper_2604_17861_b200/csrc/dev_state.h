@@ -15,7 +15,8 @@ constexpr uint64_t kQuiescent = ~0ull;  // EpochRegistry::kQuiescent (optable.hp
 constexpr uint64_t kRunning = ~0ull;    // stop_pos while running
 constexpr uint32_t kNumKinds = 80;      // module jump-table slots
 constexpr uint32_t kTaskBytes = 384;
-constexpr uint32_t kCtlBytes = 128;     // per-CTA control block after the task copy
+constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
+constexpr uint32_t kHeaderBytes = 1024;  // worker: 2 task buffers + 2 control blocks + counters
 constexpr uint32_t kScratchBytes = 96 * 1024;
 constexpr uint32_t kLaunchCounters = 1u << 16;
 
@@ -47,6 +48,10 @@ struct TraceRec {  // Tracepoint (telemetry.hpp:22-32) plus a publication stamp
   uint64_t dequeue_gt;  // device %globaltimer at claim
   uint64_t exec_ns;
   uint64_t version;
+  uint64_t t_ticket;  // phase stamps (%globaltimer): ticket taken,
+  uint64_t t_seen;    //   publication observed,
+  uint64_t t_done;    //   completion posted
+  uint64_t pad;
 };
 
 struct alignas(128) DevState {
@@ -62,7 +67,7 @@ struct alignas(128) DevState {
   uint32_t trace_on;
   uint32_t spin_iterations;
   uint32_t backoff_max_exp;
-  uint32_t pad3a;
+  uint32_t hold;       // nonzero: idle workers take no new ticket (test/handover hook)
   uint64_t pad3[12];
   // device counters (Counters, telemetry.hpp:142-196)
   uint64_t processed;

@@ -55,11 +55,17 @@ struct SharedCtl {
   uint64_t version;
   uint64_t aux;
   uint64_t t_deq;
+  uint64_t t_ticket;
+  uint64_t t_seen;
+  uint64_t t_fenced;
   uint32_t kind;
   int32_t code;
   uint32_t exit;
   uint32_t pad;
 };
+
+constexpr uint32_t kCtlStride = 112;
+static_assert(sizeof(SharedCtl) <= kCtlStride, "SharedCtl must fit its stride");
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
@@ -93,32 +99,70 @@ __device__ __forceinline__ TableEntry load_entry(const TableEntry* e) {
   return r;
 }
 
+// Host-visible per-worker counts are written lazily by warp 0 lane 0 (the
+// single writer, so posted writes stay monotone): every 16 claims and on every
+// idle poll where they changed, and once more at exit.
+struct Mirror {
+  uint64_t claimed = 0, flushed_claimed = 0, flushed_done = 0;
+};
+__device__ __forceinline__ void flush_mirror(DevState* S, uint32_t w, Mirror& m, uint64_t done) {
+  if (m.claimed != m.flushed_claimed) {
+    st_relaxed_sys(&S->host_claimed[w], m.claimed);  // claimed before done: head >= processed
+    m.flushed_claimed = m.claimed;
+  }
+  if (done != m.flushed_done) {
+    st_relaxed_sys(&S->host_done[w], done);
+    m.flushed_done = done;
+  }
+}
+
 // Warp 0: claim one ticket, wait for its publication, copy it to shared
 // memory, free the slot, and resolve the op through the versioned table.
+//
+// PCIe discipline (measured, profiles/r01_phases_*.log): every host-memory
+// access costs a round trip through the VM's PCIe path and a fence that
+// follows a sysmem store waits for it, so this path issues one slot read, one
+// slot-free store, the tail read only when the ticket is past the hint, and no
+// fence.  Task inputs need no acquire fence because the worker module is
+// compiled with -dlcm=cg: global loads bypass the (non-coherent) L1.
+//
+// Epochs: an idle worker does not park; every 16 polls it re-reads the table
+// version and republishes its epoch when the version moved, so an install's
+// epoch wait (optable.hpp:591-600) completes within a few polls while the
+// common claim path pays no system-scope fence when the version is unchanged.
 __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_task* task, SharedCtl* ctl,
-                                                uint64_t& my_epoch, uint64_t& claimed, int lane) {
+                                                uint64_t& my_epoch, Mirror& mir, const volatile uint64_t* done,
+                                                int lane) {
   uint64_t pos = 0;
-  if (lane == 0) pos = atomicAdd((unsigned long long*)&S->claim, 1ull);
+  if (lane == 0) {
+    while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
+    pos = atomicAdd((unsigned long long*)&S->claim, 1ull);
+  }
   pos = shfl64(pos, 0);
+  const uint64_t t_ticket = globaltimer();
   const char* slot = (const char*)(S->ring + (pos & S->mask));
   uint32_t spins = 0, expn = 0;
-  bool quiesced = false;
   uint4 v = make_uint4(0, 0, 0, 0);
   for (;;) {
     const uint64_t sp = ld_relaxed_gpu(&S->stop_pos);
     if (pos > sp) {
       if (lane == 0) {
         quiesce(S, w);
+        my_epoch = kQuiescent;
         ctl->exit = 1;
       }
       return;
     }
+    // Only tickets within two of the highest tail seen on the device read
+    // PCIe; the rest watch the HBM hint.  Progress: the ticket equal to the
+    // hint is always near, and its poll carries the producer tail (lane 24),
+    // so every publication eventually advances the hint.
     const uint64_t h = ld_relaxed_gpu(&S->hint);
     const bool near = pos < h + 2;
-    if (near || (spins & 7) == 0) {
+    if (near) {
       if (lane < 24) v = ld_volatile_v4(slot + 16 * lane);
       uint64_t tail = 0;
-      if (lane == 24) tail = ld_relaxed_sys(S->host_tail);
+      if (lane == 24 && pos >= h) tail = ld_relaxed_sys(S->host_tail);
       const uint64_t pub = ((uint64_t)__shfl_sync(0xffffffffu, v.y, 0) << 32) | __shfl_sync(0xffffffffu, v.x, 0);
       tail = shfl64(tail, 24);
       if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
@@ -138,33 +182,33 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
       }
     }
     ++spins;
-    if (!quiesced && spins >= S->spin_iterations) {
-      // Parked workers must not pin a table version (executor.hpp:160-161).
-      if (lane == 0) {
-        quiesce(S, w);
-        atomicAdd((unsigned long long*)&S->stalls, 1ull);
+    if (lane == 0) {
+      flush_mirror(S, w, mir, *done);  // idle: make counts visible to wait_all / peek
+      if ((spins & 15) == 0) {
+        const uint64_t ver = ld_acquire_gpu(&S->version);
+        if (ver != my_epoch) my_epoch = stable_snapshot(S, w, ver);
+        if (spins == S->spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
       }
-      quiesced = true;
-      my_epoch = kQuiescent;
     }
     if (!near) {
       __nanosleep(64u << expn);
       if (expn < S->backoff_max_exp) ++expn;
     }
   }
+  const uint64_t t_seen = globaltimer();
   // fetched: stage the descriptor in shared memory
   if (lane < 24) reinterpret_cast<uint4*>(task)[lane] = v;
   __syncwarp();
   if (lane == 0) {
-    // free the slot for the producer's next lap, then acquire: the host
-    // published the descriptor after the inputs were written.
+    // free the slot for the producer's next lap (queue.hpp:248)
     st_relaxed_sys((uint64_t*)(S->ring + (pos & S->mask)), pos + S->cap);
-    fence_acq_rel_sys();
-    ++claimed;
-    st_relaxed_sys(&S->host_claimed[w], claimed);
+    ++mir.claimed;
+    if ((mir.claimed & 15) == 0) flush_mirror(S, w, mir, *done);
+    ctl->t_fenced = globaltimer();
     ctl->pos = pos;
     ctl->exit = 0;
-    ctl->t_deq = globaltimer();
+    ctl->t_ticket = t_ticket;
+    ctl->t_seen = t_seen;
     if (task->flags & GPUOS_FLAG_SHUTDOWN) {
       atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)pos);
       quiesce(S, w);
@@ -200,15 +244,62 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
       ctl->code = code;
       ctl->kind = e.kind < kNumKinds ? e.kind : (uint32_t)GPUOS_KIND_KILLED;
       ctl->aux = e.aux;
+      ctl->t_deq = globaltimer();
     }
   }
   __syncwarp();
 }
 
+// Completion (runtime.hpp:628-639) by lane 0 of one of warps 1..7, rotating
+// per task, while warp 0 already claims the next task into the other buffer.
+// Every thread's outputs are ordered before it by the barrier; the gpu-scope
+// release puts them in L2 (where the host's copy engine reads) before the
+// word is posted.  Rotating the completer means the fence never waits on a
+// sysmem store issued by the same warp just before.
+__device__ __forceinline__ void complete_task(DevState* S, uint32_t w, const gpuos_task* task, const SharedCtl* ctl,
+                                              int code, volatile uint64_t* done, uint64_t& executed) {
+  const uint64_t t_end = globaltimer();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (task->done_cell) {
+    const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
+    st_relaxed_sys((uint64_t*)task->done_cell, word);
+  }
+  *done = *done + 1;
+  atomicAdd((unsigned long long*)&S->processed, 1ull);
+  if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);
+  atomicAdd((unsigned long long*)&S->per_op[task->op_id < 256 ? task->op_id : 255], 1ull);
+  if (S->trace_on) {
+    const uint64_t ticket = atomicAdd((unsigned long long*)&S->trace_head, 1ull);
+    TraceRec* r = &S->trace[ticket % S->trace_cap];
+    r->stamp = ticket * 2 + 1;
+    r->seq = task->seq;
+    r->op_id = task->op_id;
+    r->worker = w;
+    r->enqueue_ns = task->enqueue_ns;
+    r->dequeue_gt = ctl->t_deq;
+    r->exec_ns = t_end > ctl->t_deq ? t_end - ctl->t_deq : 1;
+    r->version = ctl->version;
+    r->t_ticket = ctl->t_ticket;
+    r->t_seen = ctl->t_seen;
+    r->t_done = globaltimer();
+    r->pad = ctl->t_fenced;
+    __threadfence();
+    r->stamp = ticket * 2 + 2;
+  }
+  ++executed;
+  const uint64_t ye = ld_relaxed_gpu(&S->yield_every);
+  if (ye > 0 && executed % ye == 0) __nanosleep(1000);  // yield_every (executor.hpp:190-193)
+}
+
 extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevState* S) {
   extern __shared__ __align__(128) char smem[];
-  gpuos_task* task = reinterpret_cast<gpuos_task*>(smem);
-  SharedCtl* ctl = reinterpret_cast<SharedCtl*>(smem + kTaskBytes);
+  // two task buffers: warp 0 fetches task k+1 while task k is being completed
+  gpuos_task* tasks[2] = {reinterpret_cast<gpuos_task*>(smem), reinterpret_cast<gpuos_task*>(smem + kTaskBytes)};
+  // header layout: task[0] | task[1] | ctl[0] | ctl[1] | done counter
+  static_assert(2 * kTaskBytes + 2 * kCtlStride + 8 <= kHeaderBytes, "worker header overflows");
+  SharedCtl* ctls[2] = {reinterpret_cast<SharedCtl*>(smem + 2 * kTaskBytes),
+                        reinterpret_cast<SharedCtl*>(smem + 2 * kTaskBytes + kCtlStride)};
+  volatile uint64_t* done = reinterpret_cast<volatile uint64_t*>(smem + 2 * kTaskBytes + 2 * kCtlStride);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t w = blockIdx.x;
   uint32_t dyn;
@@ -219,20 +310,30 @@ extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevStat
   ctx.part = 0;
   ctx.nparts = 1;
   ctx.bar_id = 1;
-  ctx.smem = smem + kTaskBytes + kCtlBytes;
-  ctx.smem_bytes = (int)dyn - (int)(kTaskBytes + kCtlBytes);
+  ctx.smem = smem + kHeaderBytes;
+  ctx.smem_bytes = (int)dyn - (int)kHeaderBytes;
   ctx.aux = 0;
   ctx.flags = 0;
-  uint64_t my_epoch = kQuiescent, claimed = 0, done = 0, executed = 0;
+  uint64_t my_epoch = kQuiescent, executed = 0;
+  Mirror mir;
   if (tid == 0) {
     // continue the host-visible counts across kernel generations
-    claimed = ld_relaxed_sys(&S->host_claimed[w]);
-    done = ld_relaxed_sys(&S->host_done[w]);
+    mir.claimed = mir.flushed_claimed = ld_relaxed_sys(&S->host_claimed[w]);
+    mir.flushed_done = ld_relaxed_sys(&S->host_done[w]);
+    *done = mir.flushed_done;
   }
-  for (;;) {
-    if (warp == 0) claim_and_fetch(S, w, task, ctl, my_epoch, claimed, lane);
+  __syncthreads();
+  const int nwarps = blockDim.x >> 5;
+  uint32_t k = 0;
+  for (;; ++k) {
+    gpuos_task* task = tasks[k & 1];
+    SharedCtl* ctl = ctls[k & 1];
+    if (warp == 0) claim_and_fetch(S, w, task, ctl, my_epoch, mir, done, lane);
     __syncthreads();
-    if (ctl->exit) return;
+    if (ctl->exit) {
+      if (tid == 0) flush_mirror(S, w, mir, *done);  // final counts for wait_all and the next generation
+      return;
+    }
     int code = ctl->code;
     if (code == GPUOS_OK) {
       ctx.aux = ctl->aux;
@@ -241,39 +342,7 @@ extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevStat
       code = fn(task, &ctx);
     }
     __syncthreads();
-    if (tid == 0) {
-      const uint64_t t_end = globaltimer();
-      // completion (runtime.hpp:628-639): outputs of every thread are ordered
-      // before the system-scope release through the barrier above.
-      fence_acq_rel_sys();
-      if (task->done_cell) {
-        const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) |
-                              (task->seq << 16);
-        st_relaxed_sys((uint64_t*)task->done_cell, word);
-      }
-      ++done;
-      st_relaxed_sys(&S->host_done[w], done);
-      atomicAdd((unsigned long long*)&S->processed, 1ull);
-      if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);
-      atomicAdd((unsigned long long*)&S->per_op[task->op_id < 256 ? task->op_id : 255], 1ull);
-      if (S->trace_on) {
-        const uint64_t ticket = atomicAdd((unsigned long long*)&S->trace_head, 1ull);
-        TraceRec* r = &S->trace[ticket % S->trace_cap];
-        r->stamp = ticket * 2 + 1;
-        r->seq = task->seq;
-        r->op_id = task->op_id;
-        r->worker = w;
-        r->enqueue_ns = task->enqueue_ns;
-        r->dequeue_gt = ctl->t_deq;
-        r->exec_ns = t_end > ctl->t_deq ? t_end - ctl->t_deq : 1;
-        r->version = ctl->version;
-        __threadfence();
-        r->stamp = ticket * 2 + 2;
-      }
-      ++executed;
-      const uint64_t ye = ld_relaxed_gpu(&S->yield_every);
-      if (ye > 0 && executed % ye == 0) __nanosleep(1000);  // yield_every (executor.hpp:190-193)
-    }
+    if (lane == 0 && warp == 1 + (int)(k % (uint32_t)(nwarps - 1))) complete_task(S, w, task, ctl, code, done, executed);
   }
 }
 
@@ -365,7 +434,7 @@ static TaskKernel task_kernel_for(uint32_t kind) {
   }
 }
 
-uint32_t worker_smem_bytes() { return kTaskBytes + kCtlBytes + kScratchBytes; }
+uint32_t worker_smem_bytes() { return kHeaderBytes + kScratchBytes; }
 
 // Lazy module loading blocks while the persistent kernel is resident
 // (measured: profiles/r01_probe2_lazy.log), so every kernel is loaded and

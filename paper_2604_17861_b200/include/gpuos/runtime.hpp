@@ -1,0 +1,762 @@
+// gpuos::Runtime — the drop-in host API (reference runtime.hpp:205-450) over
+// the B200 C-ABI.  One producer thread submits; handles may be waited on from
+// any thread (reference threading contract, runtime.hpp:5-9).
+//
+// Submission path (the north-star hot path, producer side):
+//   validate -> eligible -> reserve a ring slot -> resolve views to device
+//   addresses -> publish the 384-byte descriptor (streaming stores + release)
+//   The persistent worker kernel claims, dispatches through the dual-bank
+//   device table and posts the task's completion word, which the TaskHandle
+//   reads directly: no completion thread, no handle map, no allocation for
+//   rank <= 6 views.
+// Ineligible calls and queue-full overflow take the conventional path: one
+// cudaLaunchKernel of the same task body, synchronous (runtime.hpp:567-619).
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include <immintrin.h>
+
+#include "gpuos/bytecode.hpp"
+#include "gpuos/errors.hpp"
+#include "gpuos/expr.hpp"
+#include "gpuos/opcompiler.hpp"
+#include "gpuos/ops.hpp"
+#include "gpuos/optable.hpp"
+#include "gpuos/queue.hpp"
+#include "gpuos/telemetry.hpp"
+#include "gpuos/tensor.hpp"
+#include "gpuos_cuda.h"
+
+namespace gpuos {
+
+inline constexpr uint32_t kCompositeOpId = GPUOS_COMPOSITE_OP_ID;
+
+enum class TaskState : uint8_t { Pending = 0, Done = 1, Failed = 2 };
+
+inline const char* task_state_name(TaskState s) {
+  switch (s) {
+    case TaskState::Pending: return "Pending";
+    case TaskState::Done: return "Done";
+    case TaskState::Failed: return "Failed";
+  }
+  return "unknown";
+}
+
+inline uint64_t monotonic_ns() {
+  return static_cast<uint64_t>(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+          .count());
+}
+
+namespace detail {
+
+/// Completion cells: 8-byte words in mapped pinned memory, one per live task,
+/// written exactly once (device st.release.sys, or the host on the inline and
+/// validation paths).  Replaces HandleState (runtime.hpp:59-88).  Reference
+/// counts are host-only; a cell is reusable once unreferenced and completed.
+class CellPool {
+ public:
+  static constexpr uint32_t kBlockBits = 16;
+  static constexpr uint32_t kBlock = 1u << kBlockBits;
+
+  explicit CellPool(gpuos_dev* dev) : dev_(dev) { grow(); }
+
+  uint64_t* word(uint32_t g) const { return blocks_[g >> kBlockBits].host + (g & (kBlock - 1)); }
+  uint64_t device_addr(uint32_t g) const { return blocks_[g >> kBlockBits].dev + 8ull * (g & (kBlock - 1)); }
+
+  /// Producer thread only.  A cell is reusable when no handle references it
+  /// and its previous task's completion (tagged with that task's seq) has
+  /// landed; words are seq-tagged, so a reused cell needs no clearing store.
+  uint32_t acquire(uint64_t seq) {
+    const uint32_t total = static_cast<uint32_t>(blocks_.size()) * kBlock;
+    for (int probe = 0; probe < 64; ++probe) {
+      const uint32_t g = cursor_;
+      cursor_ = (cursor_ + 1) % total;
+      {  // the device wrote these words over PCIe: fetch them ahead of use
+        const uint32_t ahead = (g + 32) % total;
+        _mm_prefetch(reinterpret_cast<const char*>(word(ahead)), _MM_HINT_T0);
+      }
+      Block& b = blocks_[g >> kBlockBits];
+      const uint32_t i = g & (kBlock - 1);
+      if (b.refs[i].load(std::memory_order_acquire) != 0) continue;
+      const uint64_t prev = b.last_seq[i];
+      if (prev != 0) {
+        const uint64_t w = __atomic_load_n(&b.host[i], __ATOMIC_ACQUIRE);
+        if ((w & 0xffu) == 0 || (w >> 16) != (prev & kSeqMask)) continue;  // previous task in flight
+      }
+      b.last_seq[i] = seq;
+      return g;
+    }
+    cursor_ = static_cast<uint32_t>(blocks_.size()) * kBlock;
+    grow();
+    const uint32_t g = cursor_;
+    cursor_ = (cursor_ + 1) % (static_cast<uint32_t>(blocks_.size()) * kBlock);
+    blocks_[g >> kBlockBits].last_seq[g & (kBlock - 1)] = seq;
+    return g;
+  }
+  static constexpr uint64_t kSeqMask = (uint64_t{1} << 48) - 1;
+  void addref(uint32_t g) { blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_add(1, std::memory_order_relaxed); }
+  void release(uint32_t g) {
+    blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_sub(1, std::memory_order_acq_rel);
+    if (live_.fetch_sub(1, std::memory_order_acq_rel) == 1 && orphaned_.load(std::memory_order_acquire)) delete this;
+  }
+  void hold() { live_.fetch_add(1, std::memory_order_relaxed); }
+  long use_count(uint32_t g) const {
+    return static_cast<long>(blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].load(std::memory_order_relaxed));
+  }
+  /// Host-side completion (inline / validation / shutdown paths).
+  void complete(uint32_t g, uint64_t seq, ErrorCode c) {
+    const uint64_t w = (c == ErrorCode::Ok ? 1u : 2u) | (static_cast<uint64_t>(c) << 8) | (seq << 16);
+    __atomic_store_n(word(g), w, __ATOMIC_RELEASE);
+  }
+  /// Before the device memory goes away: copy words to the heap, then free
+  /// ourselves when the last handle drops.
+  void orphan() {
+    for (Block& b : blocks_) {
+      uint64_t* h = new uint64_t[kBlock];
+      std::memcpy(h, b.host, kBlock * 8);
+      b.host = h;
+      b.heap = true;
+    }
+    orphaned_.store(true, std::memory_order_release);
+    if (live_.load(std::memory_order_acquire) == 0) delete this;
+  }
+  ~CellPool() {
+    for (Block& b : blocks_) {
+      if (b.heap) delete[] b.host;
+      delete[] b.refs;
+      delete[] b.last_seq;
+    }
+  }
+
+ private:
+  struct Block {
+    uint64_t* host = nullptr;
+    uint64_t dev = 0;
+    std::atomic<uint32_t>* refs = nullptr;
+    uint64_t* last_seq = nullptr;  // seq of the cell's latest task, 0 = never used
+    bool heap = false;
+  };
+  void grow() {
+    Block b;
+    check_abi(gpuos_cells_alloc(dev_, kBlock, &b.host, &b.dev), "cells");
+    b.refs = new std::atomic<uint32_t>[kBlock]();
+    b.last_seq = new uint64_t[kBlock]();
+    blocks_.push_back(b);
+  }
+
+  gpuos_dev* dev_;
+  std::vector<Block> blocks_;
+  uint32_t cursor_ = 0;
+  std::atomic<long> live_{0};
+  std::atomic<bool> orphaned_{false};
+};
+
+}  // namespace detail
+
+/// Completion token (runtime.hpp:130-162).  Reads the task's completion word.
+class TaskHandle {
+ public:
+  TaskHandle() = default;
+  TaskHandle(const TaskHandle& o) : pool_(o.pool_), cell_(o.cell_), id_(o.id_) { ref(); }
+  TaskHandle(TaskHandle&& o) noexcept : pool_(o.pool_), cell_(o.cell_), id_(o.id_) { o.pool_ = nullptr; }
+  TaskHandle& operator=(const TaskHandle& o) {
+    if (this != &o) {
+      unref();
+      pool_ = o.pool_;
+      cell_ = o.cell_;
+      id_ = o.id_;
+      ref();
+    }
+    return *this;
+  }
+  TaskHandle& operator=(TaskHandle&& o) noexcept {
+    if (this != &o) {
+      unref();
+      pool_ = o.pool_;
+      cell_ = o.cell_;
+      id_ = o.id_;
+      o.pool_ = nullptr;
+    }
+    return *this;
+  }
+  ~TaskHandle() { unref(); }
+
+  bool valid() const { return pool_ != nullptr; }
+  uint64_t id() const {
+    check();
+    return id_;
+  }
+  TaskState state() const { return static_cast<TaskState>(raw() & 0xffu); }
+  /// Ok while Pending or Done; the failure code once Failed.
+  ErrorCode error() const {
+    const uint64_t w = raw();
+    if ((w & 0xffu) != static_cast<uint64_t>(TaskState::Failed)) return ErrorCode::Ok;
+    return static_cast<ErrorCode>((w >> 8) & 0xffu);
+  }
+  /// Block until terminal: spin, then yield, then sleep.
+  TaskState wait() const {
+    uint64_t w = raw();
+    for (uint32_t spin = 0; (w & 0xffu) == 0; ++spin) {
+      if (spin < 2048) {
+        __builtin_ia32_pause();
+      } else if (spin < 4096) {
+        std::this_thread::yield();
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(10));
+      }
+      w = raw();
+    }
+    return static_cast<TaskState>(w & 0xffu);
+  }
+  long use_count() const { return pool_ ? pool_->use_count(cell_) : 0; }
+
+ private:
+  friend class Runtime;
+  TaskHandle(detail::CellPool* p, uint32_t cell, uint64_t id) : pool_(p), cell_(cell), id_(id) { ref(); }
+  void check() const {
+    if (!pool_) throw Error(ErrorCode::Internal, "operation on an invalid task handle");
+  }
+  // The cell word belongs to this task only when its seq tag matches.
+  uint64_t raw() const {
+    check();
+    const uint64_t w = __atomic_load_n(pool_->word(cell_), __ATOMIC_ACQUIRE);
+    return (w >> 16) == (id_ & detail::CellPool::kSeqMask) ? w : 0;
+  }
+  void ref() {
+    if (pool_) {
+      pool_->hold();
+      pool_->addref(cell_);
+    }
+  }
+  void unref() {
+    if (pool_) pool_->release(cell_);
+    pool_ = nullptr;
+  }
+  detail::CellPool* pool_ = nullptr;
+  uint32_t cell_ = 0;
+  uint64_t id_ = 0;
+};
+
+struct OpCall {
+  uint64_t op_id = 0;
+  std::vector<TensorView> inputs;
+  TensorView output;
+  std::vector<double> scalars;
+};
+
+struct WorkerConfig {
+  size_t num_workers = 0;         // worker CTAs; 0 = one per SM
+  uint64_t yield_every = 0;       // executor.hpp:28
+  uint32_t spin_iterations = 64;  // executor.hpp:29
+  uint32_t backoff_max_exp = 6;   // nanosleep ladder 64 ns * 2^k
+};
+
+struct RuntimeConfig {
+  size_t capacity = 4096;
+  WorkerConfig workers;
+  uint64_t max_elements = 65536;
+  int64_t max_sdpa_context = 2048;
+  bool fusion_enabled = false;
+  size_t max_chain = 8;
+  size_t table_slots = 1024;
+  size_t trace_capacity = 65536;
+  bool telemetry_enabled = true;
+  int device = 0;
+  /// Route matmul_small / vecmat (dims <= 256) to the persistent workers.  The
+  /// reference never queues them (runtime.hpp:531-534); config 3 needs them
+  /// queued, so this build defaults to true.
+  bool queue_matmul = true;
+
+  /// GPUOS_CAPACITY, GPUOS_WORKERS, GPUOS_YIELD_EVERY, GPUOS_MAX_ELEMS, GPUOS_DEVICE.
+  static RuntimeConfig from_env() {
+    RuntimeConfig c;
+    c.capacity = static_cast<size_t>(env_u64("GPUOS_CAPACITY", c.capacity));
+    c.workers.num_workers = static_cast<size_t>(env_u64("GPUOS_WORKERS", c.workers.num_workers));
+    c.workers.yield_every = env_u64("GPUOS_YIELD_EVERY", c.workers.yield_every);
+    c.max_elements = env_u64("GPUOS_MAX_ELEMS", c.max_elements);
+    c.device = static_cast<int>(env_u64("GPUOS_DEVICE", static_cast<uint64_t>(c.device)));
+    return c;
+  }
+
+ private:
+  static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* s = std::getenv(name);
+    if (!s || !*s) return dflt;
+    char* end = nullptr;
+    const unsigned long long v = std::strtoull(s, &end, 10);
+    return (end == s || *end != '\0') ? dflt : static_cast<uint64_t>(v);
+  }
+};
+
+class Runtime {
+ public:
+  explicit Runtime(RuntimeConfig cfg = {}) : cfg_(normalize(std::move(cfg))) {
+    if (cfg_.capacity == 0) throw Error(ErrorCode::ZeroCapacity, "queue capacity must be positive");
+    gpuos_cfg c{};
+    gpuos_default_cfg(&c);
+    c.capacity = cfg_.capacity;
+    c.table_slots = static_cast<uint32_t>(cfg_.table_slots);
+    c.num_workers = static_cast<uint32_t>(cfg_.workers.num_workers);
+    c.spin_iterations = cfg_.workers.spin_iterations;
+    c.backoff_max_exp = cfg_.workers.backoff_max_exp;
+    c.yield_every = cfg_.workers.yield_every;
+    c.trace_capacity = cfg_.trace_capacity;
+    c.telemetry = cfg_.telemetry_enabled ? 1u : 0u;
+    check_abi(gpuos_dev_open(cfg_.device, &c, &dev_), "gpuos_dev_open");
+    pool_ = std::make_unique<BufferPool>(dev_);
+    table_ = std::make_unique<OperatorTable>(dev_);
+    cells_ = new detail::CellPool(dev_);
+    counters_ = std::make_unique<Counters>(cfg_.table_slots < 256 ? cfg_.table_slots : 256);
+    check_abi(gpuos_stream_create(dev_, &inline_stream_), "inline stream");
+    // builtins at their fixed ids, then the composite handler: version 15
+    // after construction, as in the reference (test_runtime.cpp:61-62).
+    for (uint32_t i = 0; i < kNumBuiltinOps; ++i) {
+      InjectionRecord meta;
+      meta.template_name = "builtin";
+      meta.signature = op_kind_name(static_cast<OpKind>(i));
+      table_->install_builtin(i, static_cast<OpKind>(i), std::move(meta));
+    }
+    InjectionRecord cm;
+    cm.template_name = "builtin";
+    cm.signature = "composite";
+    table_->install_program(kCompositeOpId, composite_placeholder(), 1, DType::F64, std::move(cm));
+    fusion_on_ = cfg_.fusion_enabled;
+  }
+
+  ~Runtime() {
+    shutdown();
+    if (inline_stream_) gpuos_stream_destroy(dev_, inline_stream_);
+    table_.reset();
+    pool_.reset();
+    cells_->orphan();
+    gpuos_dev_close(dev_);
+  }
+
+  Runtime(const Runtime&) = delete;
+  Runtime& operator=(const Runtime&) = delete;
+
+  // ---- tensors ----
+  BufferPool& pool() { return *pool_; }
+  TensorView alloc_tensor(DType dtype, Shape shape) {
+    TensorView v;
+    v.dtype = dtype;
+    v.shape = std::move(shape);
+    v.strides = contiguous_strides(v.shape);
+    v.buffer = pool_->allocate(dtype, static_cast<size_t>(v.numel()));
+    return v;
+  }
+
+  // ---- submission (never throws; failures land on the handle) ----
+  TaskHandle submit(uint64_t op_id, std::vector<TensorView> inputs, TensorView output,
+                    std::vector<double> scalars = {}) {
+    return submit_span(op_id, inputs, output, scalars);
+  }
+  TaskHandle submit(OpKind kind, std::vector<TensorView> inputs, TensorView output, std::vector<double> scalars = {}) {
+    return submit_span(static_cast<uint64_t>(kind), inputs, output, scalars);
+  }
+  /// Braced-list fast path: `rt.submit(OpKind::Add, {a, b}, c)` allocates nothing.
+  TaskHandle submit(OpKind kind, std::initializer_list<TensorView> inputs, const TensorView& output,
+                    std::initializer_list<double> scalars = {}) {
+    return submit_span(static_cast<uint64_t>(kind), std::span<const TensorView>(inputs.begin(), inputs.size()), output,
+                       std::span<const double>(scalars.begin(), scalars.size()));
+  }
+  TaskHandle submit(uint64_t op_id, std::initializer_list<TensorView> inputs, const TensorView& output,
+                    std::initializer_list<double> scalars = {}) {
+    return submit_span(op_id, std::span<const TensorView>(inputs.begin(), inputs.size()), output,
+                       std::span<const double>(scalars.begin(), scalars.size()));
+  }
+  TaskHandle submit(const OpCall& call) { return submit_span(call.op_id, call.inputs, call.output, call.scalars); }
+
+  TaskHandle submit_span(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+                         std::span<const double> scalars) {
+    const uint64_t id = next_id_++;
+    const uint32_t cell = cells_->acquire(id);
+    TaskHandle h(cells_, cell, id);
+    if (stopped_) {
+      counters_->inc_failed();
+      cells_->complete(cell, id, ErrorCode::RuntimeStopped);
+      return h;
+    }
+    if (const ErrorCode v = validate(inputs, output, scalars); v != ErrorCode::Ok) {
+      counters_->inc_failed();  // not counted as submitted (runtime.hpp:261-265)
+      cells_->complete(cell, id, v);
+      return h;
+    }
+    counters_->inc_submitted();
+    const bool elig = eligible(op_id, inputs, output);
+    route(op_id, inputs, output, scalars, cell, id, elig, 0);
+    return h;
+  }
+
+  // ---- fusion (next row of SURVEY §8(f); the chain is not fused yet) ----
+  void set_fusion(bool on) { fusion_on_ = on; }
+  bool fusion() const { return fusion_on_; }
+  void fuse() {}
+  std::vector<TaskHandle> fuse(std::span<const OpCall> calls) {
+    std::vector<TaskHandle> out;
+    out.reserve(calls.size());
+    for (const OpCall& c : calls) {
+      out.push_back(submit(c));
+      wait(out.back());  // sequential semantics: each step observes the previous
+    }
+    return out;
+  }
+  uint64_t fusion_absorbed() const { return 0; }
+
+  // ---- injection ----
+  uint64_t inject_operator(const std::string& template_name, std::span<const double> params = {},
+                           DType dtype = DType::F32) {
+    if (next_injected_id_ >= table_->slots()) throw Error(ErrorCode::TableFull, "no free injected op ids");
+    return inject_operator_at(static_cast<uint32_t>(next_injected_id_), template_name, params, dtype);
+  }
+  uint64_t inject_operator_at(uint32_t op_id, const std::string& template_name, std::span<const double> params = {},
+                              DType dtype = DType::F32) {
+    if (stopped_) throw Error(ErrorCode::RuntimeStopped, "inject after shutdown");
+    if (op_id < kFirstInjectedId)
+      throw Error(ErrorCode::OutOfRange, "injected ids start at " + std::to_string(kFirstInjectedId));
+    if (op_id >= table_->slots())
+      throw Error(ErrorCode::OutOfRange, "op id " + std::to_string(op_id) + " past table size");
+    const OperatorTemplate tmpl = registry_.get(template_name);
+    const uint64_t h0 = cache_.hits(), m0 = cache_.misses();
+    ModulePtr mod;
+    try {
+      mod = cache_.compile_or_get(tmpl, params, dtype);
+    } catch (...) {
+      sync_cache_counters(h0, m0);
+      throw;
+    }
+    sync_cache_counters(h0, m0);
+    InjectionRecord meta;
+    meta.template_name = template_name;
+    meta.params.assign(params.begin(), params.end());
+    meta.signature = signature_key(mod->signature);
+    last_inject_ = table_->install_program(op_id, mod->bytecode, mod->signature.arity, dtype, std::move(meta));
+    modules_by_id_[op_id] = mod;
+    counters_->inc_injections();
+    if (op_id >= next_injected_id_) next_injected_id_ = static_cast<uint64_t>(op_id) + 1;
+    return op_id;
+  }
+  void kill_operator(uint32_t op_id) {
+    if (stopped_) throw Error(ErrorCode::RuntimeStopped, "kill after shutdown");
+    table_->kill(op_id);
+    modules_by_id_.erase(op_id);  // killed injected ops leave the eligible set
+  }
+  /// Timings of the most recent injection's upload / epoch wait / bank write / flip.
+  const gpuos_inject_stats& last_inject_stats() const { return last_inject_; }
+
+  TemplateRegistry& templates() { return registry_; }
+  OperatorTable& table() { return *table_; }
+  ModuleCache& module_cache() { return cache_; }
+
+  // ---- completion / introspection ----
+  TaskState wait(const TaskHandle& h) { return h.wait(); }
+  void wait_all() {
+    const int rc = gpuos_ring_wait_processed(dev_, committed_tasks_);
+    if (rc != 0 && rc != static_cast<int>(ErrorCode::RuntimeStopped)) check_abi(rc, "wait_all");
+  }
+  TaskQueue::Snapshot peek_queue() const {
+    gpuos_snapshot s{};
+    gpuos_ring_peek(dev_, &s);
+    return TaskQueue::Snapshot{s.head, s.tail, s.processed};
+  }
+  CounterSnapshot counters() const {
+    CounterSnapshot s = counters_->snapshot();
+    gpuos_dev_stats d{};
+    if (gpuos_dev_get_stats(dev_, &d) == 0) {
+      s.processed = d.processed;
+      s.stalls = d.stalls;
+      s.failed += d.failed;
+      for (size_t i = 0; i < 256; ++i) {
+        if (!d.per_op[i]) continue;
+        const size_t b = std::min(i, s.per_op.size() - 1);
+        s.per_op[b] += d.per_op[i];
+      }
+    }
+    return s;
+  }
+  std::vector<Tracepoint> trace() const {
+    std::vector<gpuos_tracepoint> raw(cfg_.trace_capacity ? cfg_.trace_capacity : 1);
+    uint64_t n = 0;
+    gpuos_trace_snapshot(dev_, raw.data(), raw.size(), &n);
+    std::vector<Tracepoint> out;
+    out.reserve(n + inline_trace_.size());
+    for (uint64_t i = 0; i < n; ++i) {
+      Tracepoint t;
+      t.seq = raw[i].seq;
+      t.op_id = raw[i].op_id;
+      t.worker = raw[i].worker;
+      t.enqueue_ns = raw[i].enqueue_ns;
+      t.dequeue_ns = raw[i].dequeue_ns;
+      t.exec_ns = raw[i].exec_ns;
+      t.version = raw[i].version;
+      out.push_back(t);
+    }
+    {
+      std::lock_guard<std::mutex> lk(trace_mu_);
+      out.insert(out.end(), inline_trace_.begin(), inline_trace_.end());
+    }
+    std::stable_sort(out.begin(), out.end(),
+                     [](const Tracepoint& a, const Tracepoint& b) { return a.enqueue_ns < b.enqueue_ns; });
+    if (out.size() > cfg_.trace_capacity) out.erase(out.begin(), out.end() - static_cast<long>(cfg_.trace_capacity));
+    return out;
+  }
+
+  bool worker_alive() const { return gpuos_dev_alive(dev_) != 0; }
+  size_t num_workers() const {
+    uint32_t n = 0;
+    gpuos_dev_num_workers(dev_, &n);
+    return n;
+  }
+  uint64_t canary_hits() const {
+    gpuos_dev_stats d{};
+    return gpuos_dev_get_stats(dev_, &d) == 0 ? d.canary_hits : 0;
+  }
+  void set_yield_every(uint64_t n) { gpuos_set_yield_every(dev_, n); }
+  bool stopped() const { return stopped_; }
+  size_t pending_composites() const { return 0; }
+  gpuos_dev* device() const { return dev_; }
+  const RuntimeConfig& config() const { return cfg_; }
+
+  /// Drain, stop the worker kernel, release all buffers; idempotent.
+  void shutdown() {
+    if (stopped_) return;
+    wait_all();
+    stopped_ = true;
+    gpuos_dev_stop(dev_);
+    pool_->clear();
+  }
+
+  /// Benchmark hook: drain and stop the worker kernel, then relaunch it (the
+  /// ring, table and buffers persist).  Lets a timed step bracket one whole
+  /// kernel lifetime with CUDA events.
+  void restart_workers() {
+    wait_all();
+    check_abi(gpuos_dev_stop(dev_), "stop");
+    check_abi(gpuos_dev_start(dev_), "start");
+  }
+
+ private:
+  static RuntimeConfig normalize(RuntimeConfig cfg) {
+    if (cfg.max_chain == 0) cfg.max_chain = 1;
+    if (cfg.table_slots < kFirstInjectedId + 1) cfg.table_slots = kFirstInjectedId + 1;
+    return cfg;
+  }
+
+  // The composite slot (id 31) holds an identity program until fusion lands.
+  static Bytecode composite_placeholder() { return {{OpCode::LoadIn, 0, 0.0}, {OpCode::StoreOut, 0, 0.0}}; }
+
+  static ErrorCode validate(std::span<const TensorView> inputs, const TensorView& output,
+                            std::span<const double> scalars) {
+    if (inputs.size() > kMaxInputs || scalars.size() > kMaxScalars) return ErrorCode::ArityError;
+    if (output.buffer == kInvalidBuffer) return ErrorCode::InvalidBuffer;
+    if (output.strides.size() != output.shape.size()) return ErrorCode::IncompatibleShapes;
+    for (const TensorView& v : inputs) {
+      if (v.buffer == kInvalidBuffer) return ErrorCode::InvalidBuffer;
+      if (v.strides.size() != v.shape.size()) return ErrorCode::IncompatibleShapes;
+    }
+    return ErrorCode::Ok;
+  }
+
+  static uint64_t work_elements(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output) {
+    if (op_id < kNumBuiltinOps) {
+      switch (static_cast<OpKind>(op_id)) {
+        case OpKind::ReduceSum: case OpKind::ReduceMax: case OpKind::ReduceMin:
+          return inputs.empty() ? 0 : static_cast<uint64_t>(inputs[0].numel());
+        case OpKind::Sdpa:
+          return inputs.size() >= 2 ? static_cast<uint64_t>(inputs[1].numel()) : 0;
+        case OpKind::KvAppend:
+          return inputs.size() >= 2 ? static_cast<uint64_t>(inputs[0].numel() + inputs[1].numel()) : 0;
+        default: break;
+      }
+    }
+    return static_cast<uint64_t>(output.numel());
+  }
+
+  /// Routing filter (runtime.hpp:503-538), with matmul/vecmat queued when
+  /// cfg_.queue_matmul (their own 256 cap then applies on the worker).
+  bool eligible(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output) const {
+    bool kind_ok = false;
+    if (op_id >= kFirstInjectedId) {
+      kind_ok = op_id <= UINT32_MAX && modules_by_id_.count(static_cast<uint32_t>(op_id)) != 0;
+    } else if (op_id < kNumBuiltinOps) {
+      switch (static_cast<OpKind>(op_id)) {
+        case OpKind::Sdpa:
+          kind_ok = inputs.size() >= 2 && inputs[1].rank() == 3 && inputs[1].shape[1] <= cfg_.max_sdpa_context;
+          break;
+        case OpKind::MatMulSmall: case OpKind::VecMat:
+          kind_ok = cfg_.queue_matmul;
+          break;
+        default:
+          kind_ok = true;
+      }
+    }
+    return kind_ok && work_elements(op_id, inputs, output) <= cfg_.max_elements;
+  }
+
+  // Resolve a view to the device descriptor (BoundView's checks move here,
+  // reported by the body at the reference's bind point).
+  bool bind(const TensorView& v, gpuos_view* out) const {
+    if (v.rank() > GPUOS_MAX_RANK) return false;
+    out->dtype = static_cast<uint8_t>(v.dtype);
+    out->rank = static_cast<uint8_t>(v.rank());
+    out->status = GPUOS_VIEW_OK;
+    out->reserved = 0;
+    out->buffer_lo = static_cast<uint32_t>(v.buffer);
+    out->addr = 0;
+    int64_t lo = v.offset, hi = v.offset, n = 1;
+    for (size_t d = 0; d < v.rank(); ++d) {
+      const int64_t e = v.shape[d], s = v.strides[d];
+      if (e < 0 || e > INT32_MAX || s > INT32_MAX || s < INT32_MIN) return false;
+      out->extents[d] = static_cast<int32_t>(e);
+      out->strides[d] = static_cast<int32_t>(s);
+      n *= e;
+      if (e > 0) (s > 0 ? hi : lo) += (e - 1) * s;
+    }
+    for (size_t d = v.rank(); d < GPUOS_MAX_RANK; ++d) out->extents[d] = out->strides[d] = 0;
+    const BufferPool::Buffer* b = pool_->find(v.buffer);
+    if (!b) {
+      out->status = GPUOS_VIEW_UNKNOWN_BUFFER;
+    } else if (b->dtype != v.dtype) {
+      out->status = GPUOS_VIEW_DTYPE_VS_BUFFER;
+    } else if (n > 0 && (lo < 0 || hi >= static_cast<int64_t>(b->length))) {
+      out->status = GPUOS_VIEW_OUT_OF_BOUNDS;
+    } else {
+      out->addr = reinterpret_cast<uint64_t>(static_cast<char*>(b->data) + v.offset * static_cast<int64_t>(dtype_width(v.dtype)));
+    }
+    return true;
+  }
+
+  bool build_task(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+                  std::span<const double> scalars, uint32_t cell, uint64_t id, uint16_t flags, gpuos_task* t) const {
+    t->pub = 0;
+    t->seq = id;
+    t->op_id = static_cast<uint32_t>(op_id);
+    t->flags = flags;
+    t->n_inputs = static_cast<uint8_t>(inputs.size());
+    t->n_scalars = static_cast<uint8_t>(scalars.size());
+    t->size = static_cast<uint64_t>(output.numel());
+    t->done_cell = cells_->device_addr(cell);
+    t->enqueue_ns = 0;
+    t->aux = 0;
+    t->checksum = 0;
+    for (size_t i = 0; i < kMaxScalars; ++i) t->scalars[i] = i < scalars.size() ? scalars[i] : 0.0;
+    if (!bind(output, &t->views[0])) return false;
+    for (size_t i = 0; i < inputs.size(); ++i)
+      if (!bind(inputs[i], &t->views[1 + i])) return false;
+    for (size_t i = inputs.size(); i < kMaxInputs; ++i) std::memset(&t->views[1 + i], 0, sizeof(gpuos_view));
+    t->reserved2[0] = t->reserved2[1] = 0;
+    return true;
+  }
+
+  void route(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+             std::span<const double> scalars, uint32_t cell, uint64_t id, bool elig, uint16_t flags) {
+    // Views of rank > 4 or with extents/strides beyond int32 do not fit a
+    // slot (the reference spills them, queue.hpp:207-221); they take the
+    // conventional path, which reports TooLarge for them.
+    alignas(64) gpuos_task t;
+    if (elig && op_id <= UINT32_MAX && build_task(op_id, inputs, output, scalars, cell, id, flags, &t)) {
+      uint64_t pos = 0;
+      if (gpuos_ring_reserve(dev_, &pos) == 0) {
+        gpuos_ring_publish(dev_, pos, &t);
+        counters_->inc_committed();
+        ++committed_tasks_;
+        return;
+      }
+      counters_->inc_queue_full_fallback();
+    }
+    execute_inline(op_id, inputs, output, scalars, cell, id);
+  }
+
+  void execute_inline(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+                      std::span<const double> scalars, uint32_t cell, uint64_t id) {
+    counters_->inc_inline();
+    const uint64_t t0 = monotonic_ns();
+    ErrorCode code = ErrorCode::Ok;
+    if (op_id >= table_->slots()) {
+      code = ErrorCode::OutOfRange;
+    } else {
+      const OperatorEntry e = table_->latest_entry(op_id);
+      if (e.status == OpStatus::Empty) code = ErrorCode::NotInstalled;
+      else if (e.status == OpStatus::Killed) code = ErrorCode::OperatorKilled;
+    }
+    if (code == ErrorCode::Ok) {
+      // matmuls run uncapped on the conventional path (runtime.hpp:589-594)
+      const uint16_t flags = (op_id == static_cast<uint64_t>(OpKind::MatMulSmall) ||
+                              op_id == static_cast<uint64_t>(OpKind::VecMat))
+                                 ? GPUOS_FLAG_UNCAPPED
+                                 : 0;
+      alignas(64) gpuos_task t;
+      if (!build_task(op_id, inputs, output, scalars, cell, id, flags, &t)) {
+        code = ErrorCode::TooLarge;
+      } else {
+        int rc = gpuos_launch_task(dev_, &t, inline_stream_);
+        if (rc == 0) rc = gpuos_stream_sync(dev_, inline_stream_);
+        if (rc != 0) {
+          code = static_cast<ErrorCode>(rc);
+        } else {
+          const uint64_t w = __atomic_load_n(cells_->word(cell), __ATOMIC_ACQUIRE);
+          code = (w & 0xffu) == 1 ? ErrorCode::Ok : static_cast<ErrorCode>((w >> 8) & 0xffu);
+        }
+      }
+    }
+    uint64_t t1 = monotonic_ns();
+    if (t1 <= t0) t1 = t0 + 1;
+    if (code != ErrorCode::Ok) counters_->inc_failed();
+    counters_->inc_op(op_id);
+    if (cfg_.telemetry_enabled) {
+      Tracepoint tp;
+      tp.seq = id;
+      tp.op_id = op_id;
+      tp.worker = 0xFFFFFFFFu;
+      tp.enqueue_ns = t0;
+      tp.dequeue_ns = t0;
+      tp.exec_ns = t1 - t0;
+      tp.version = table_->snapshot_version();
+      std::lock_guard<std::mutex> lk(trace_mu_);
+      inline_trace_.push_back(tp);
+      if (inline_trace_.size() > cfg_.trace_capacity) inline_trace_.erase(inline_trace_.begin());
+    }
+    cells_->complete(cell, id, code);
+  }
+
+  void sync_cache_counters(uint64_t h0, uint64_t m0) {
+    for (uint64_t k = cache_.hits() - h0; k > 0; --k) counters_->inc_cache_hit();
+    for (uint64_t k = cache_.misses() - m0; k > 0; --k) counters_->inc_cache_miss();
+  }
+
+  RuntimeConfig cfg_;
+  gpuos_dev* dev_ = nullptr;
+  std::unique_ptr<BufferPool> pool_;
+  std::unique_ptr<OperatorTable> table_;
+  detail::CellPool* cells_ = nullptr;
+  std::unique_ptr<Counters> counters_;
+  ModuleCache cache_;
+  TemplateRegistry registry_ = TemplateRegistry::with_defaults();
+  void* inline_stream_ = nullptr;
+  bool stopped_ = false;
+  bool fusion_on_ = false;
+  uint64_t next_id_ = 1;
+  uint64_t committed_tasks_ = 0;
+  uint64_t next_injected_id_ = kFirstInjectedId;
+  std::unordered_map<uint32_t, ModulePtr> modules_by_id_;
+  gpuos_inject_stats last_inject_{};
+  mutable std::mutex trace_mu_;
+  std::vector<Tracepoint> inline_trace_;
+};
+
+}  // namespace gpuos

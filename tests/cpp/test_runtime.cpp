@@ -1,0 +1,572 @@
+// Runtime parity suite on the B200 (restates reference tests/test_runtime.cpp,
+// test_executor.cpp and acceptance criteria C2/C3/C7 against gpuos::Runtime):
+// lifecycle, routing, overflow fallback, injection and kill, error codes,
+// queue-vs-inline equivalence, accounting identities, hot-swap under load,
+// drain-on-shutdown.  Built by `make cpp-tests`, run by tests/test_cpp_gpu.py.
+#include <gpuos/runtime.hpp>
+
+#include <cmath>
+#include <cstdlib>
+#include <random>
+#include <sstream>
+#include <thread>
+#include <vector>
+
+#include "check.hpp"
+
+using namespace gpuos;
+
+namespace {
+
+bool close_tol(double got, double want, double tol) {
+  if (std::isnan(got) || std::isnan(want)) return std::isnan(got) && std::isnan(want);
+  return std::abs(got - want) <= tol * std::max(1.0, std::abs(want));
+}
+
+std::vector<double> read_all(Runtime& rt, const TensorView& v) {
+  BoundView b(rt.pool(), v);
+  std::vector<double> out(static_cast<size_t>(v.numel()));
+  for (size_t i = 0; i < out.size(); ++i) out[i] = b.load(static_cast<int64_t>(i));
+  return out;
+}
+
+void fill(Runtime& rt, const TensorView& v, const std::vector<double>& vals) {
+  BoundView b(rt.pool(), v);
+  for (size_t i = 0; i < vals.size(); ++i) b.store(static_cast<int64_t>(i), vals[i]);
+}
+
+std::vector<double> random_vals(std::mt19937_64& rng, size_t n, double lo = -4.0, double hi = 4.0) {
+  std::uniform_real_distribution<double> d(lo, hi);
+  std::vector<double> v(n);
+  for (double& x : v) x = d(rng);
+  return v;
+}
+
+RuntimeConfig small_config(size_t capacity = 256, size_t workers = 8) {
+  RuntimeConfig c;
+  c.capacity = capacity;
+  c.workers.num_workers = workers;
+  return c;
+}
+
+double f32(double x) { return static_cast<double>(static_cast<float>(x)); }
+
+}  // namespace
+
+TEST_CASE("config from env") {
+  ::setenv("GPUOS_CAPACITY", "128", 1);
+  ::setenv("GPUOS_WORKERS", "3", 1);
+  ::setenv("GPUOS_YIELD_EVERY", "5", 1);
+  ::setenv("GPUOS_MAX_ELEMS", "1000", 1);
+  RuntimeConfig env = RuntimeConfig::from_env();
+  CHECK(env.capacity == 128);
+  CHECK(env.workers.num_workers == 3);
+  CHECK(env.workers.yield_every == 5);
+  CHECK(env.max_elements == 1000);
+  ::setenv("GPUOS_CAPACITY", "not-a-number", 1);
+  ::setenv("GPUOS_WORKERS", "", 1);
+  ::setenv("GPUOS_MAX_ELEMS", "12x", 1);
+  env = RuntimeConfig::from_env();
+  CHECK(env.capacity == 4096);
+  CHECK(env.workers.num_workers == 0);
+  CHECK(env.max_elements == 65536);
+  ::unsetenv("GPUOS_CAPACITY");
+  ::unsetenv("GPUOS_WORKERS");
+  ::unsetenv("GPUOS_YIELD_EVERY");
+  ::unsetenv("GPUOS_MAX_ELEMS");
+  const RuntimeConfig d;
+  CHECK(d.capacity == 4096);
+  CHECK(d.max_elements == 65536);
+  CHECK(d.max_chain == 8);
+  CHECK(d.max_sdpa_context == 2048);
+  CHECK_FALSE(d.fusion_enabled);
+}
+
+TEST_CASE("runtime starts with the builtin set at version 15") {
+  Runtime rt(small_config(256, 2));
+  REQUIRE(rt.worker_alive());
+  REQUIRE(rt.num_workers() == 2);
+  REQUIRE_FALSE(rt.stopped());
+  REQUIRE(rt.table().snapshot_version() == kNumBuiltinOps + 1);
+  REQUIRE(rt.table().latest_entry(static_cast<uint64_t>(OpKind::Relu)).status == OpStatus::Active);
+  REQUIRE(rt.table().latest_entry(kCompositeOpId).status == OpStatus::Active);
+  REQUIRE(rt.table().latest_entry(40).status == OpStatus::Empty);
+  const TaskQueue::Snapshot s = rt.peek_queue();
+  REQUIRE(s.head == 0);
+  REQUIRE(s.tail == 0);
+  REQUIRE(s.processed == 0);
+}
+
+TEST_CASE("init, shutdown, init again leaves no residue") {
+  for (int round = 0; round < 2; ++round) {
+    Runtime rt(small_config(16, 2));
+    REQUIRE(rt.worker_alive());
+    auto a = rt.alloc_tensor(DType::F32, {32});
+    auto out = rt.alloc_tensor(DType::F32, {32});
+    fill(rt, a, std::vector<double>(32, 2.0));
+    auto h = rt.submit(OpKind::Relu, {a}, out);
+    REQUIRE(rt.wait(h) == TaskState::Done);
+    rt.shutdown();
+    REQUIRE_FALSE(rt.worker_alive());
+    REQUIRE(rt.stopped());
+    rt.shutdown();
+    auto late = rt.submit(OpKind::Relu, {a}, out);
+    REQUIRE(late.state() == TaskState::Failed);
+    REQUIRE(late.error() == ErrorCode::RuntimeStopped);
+  }
+}
+
+TEST_CASE("small elementwise work routes to the persistent workers, bit-exact") {
+  Runtime rt(small_config());
+  std::mt19937_64 rng(101);
+  auto a = rt.alloc_tensor(DType::F32, {1024});
+  auto b = rt.alloc_tensor(DType::F32, {1024});
+  auto out = rt.alloc_tensor(DType::F32, {1024});
+  const auto va = random_vals(rng, 1024), vb = random_vals(rng, 1024);
+  fill(rt, a, va);
+  fill(rt, b, vb);
+  auto h = rt.submit(OpKind::Add, {a, b}, out);
+  REQUIRE(rt.wait(h) == TaskState::Done);
+  const CounterSnapshot c = rt.counters();
+  CHECK(c.submitted == 1);
+  CHECK(c.committed == 1);
+  CHECK(c.inline_executions == 0);
+  CHECK(c.processed == 1);
+  const auto got = read_all(rt, out);
+  for (size_t i = 0; i < got.size(); ++i) REQUIRE(got[i] == f32(f32(va[i]) + f32(vb[i])));
+}
+
+TEST_CASE("large matmul executes inline on the conventional path") {
+  Runtime rt(small_config());
+  std::mt19937_64 rng(202);
+  const int64_t n = 512;
+  auto a = rt.alloc_tensor(DType::F32, {n, n});
+  auto b = rt.alloc_tensor(DType::F32, {n, n});
+  auto out = rt.alloc_tensor(DType::F32, {n, n});
+  const auto va = random_vals(rng, static_cast<size_t>(n * n), -1.0, 1.0);
+  const auto vb = random_vals(rng, static_cast<size_t>(n * n), -1.0, 1.0);
+  fill(rt, a, va);
+  fill(rt, b, vb);
+  auto h = rt.submit(OpKind::MatMulSmall, {a, b}, out);
+  REQUIRE(h.state() == TaskState::Done);  // inline is synchronous
+  const CounterSnapshot c = rt.counters();
+  CHECK(c.inline_executions == 1);
+  CHECK(c.committed == 0);
+  BoundView bo(rt.pool(), out);
+  std::uniform_int_distribution<int64_t> pick(0, n - 1);
+  for (int t = 0; t < 12; ++t) {
+    const int64_t i = pick(rng), j = pick(rng);
+    double want = 0.0;
+    for (int64_t k = 0; k < n; ++k) want += f32(va[static_cast<size_t>(i * n + k)]) * f32(vb[static_cast<size_t>(k * n + j)]);
+    REQUIRE(close_tol(bo.load(i * n + j), want, 1e-6));
+  }
+}
+
+TEST_CASE("small matmul is queued and bit-exact against double ascending-k") {
+  Runtime rt(small_config());
+  std::mt19937_64 rng(203);
+  const int64_t m = 128, k = 64, n = 128;
+  auto a = rt.alloc_tensor(DType::F32, {m, k});
+  auto kt = rt.alloc_tensor(DType::F32, {n, k});  // K, used transposed
+  auto out = rt.alloc_tensor(DType::F32, {m, n});
+  const auto va = random_vals(rng, static_cast<size_t>(m * k), -1.0, 1.0);
+  const auto vk = random_vals(rng, static_cast<size_t>(n * k), -1.0, 1.0);
+  fill(rt, a, va);
+  fill(rt, kt, vk);
+  TensorView kview = kt;  // (k, n) view of K with strides swapped
+  kview.shape = {k, n};
+  kview.strides = {1, k};
+  REQUIRE(rt.wait(rt.submit(OpKind::MatMulSmall, {a, kview}, out)) == TaskState::Done);
+  CHECK(rt.counters().committed == 1);
+  const auto got = read_all(rt, out);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int64_t p = 0; p < k; ++p) acc += f32(va[static_cast<size_t>(i * k + p)]) * f32(vk[static_cast<size_t>(j * k + p)]);
+      REQUIRE(got[static_cast<size_t>(i * n + j)] == f32(acc));
+    }
+}
+
+TEST_CASE("work ceiling splits routing at the element boundary") {
+  RuntimeConfig cfg = small_config();
+  cfg.max_elements = 4096;
+  Runtime rt(cfg);
+  auto si = rt.alloc_tensor(DType::F32, {4096});
+  auto so = rt.alloc_tensor(DType::F32, {4096});
+  auto bi = rt.alloc_tensor(DType::F32, {4097});
+  auto bo = rt.alloc_tensor(DType::F32, {4097});
+  fill(rt, si, std::vector<double>(4096, -1.5));
+  fill(rt, bi, std::vector<double>(4097, -1.5));
+  rt.wait(rt.submit(OpKind::Relu, {si}, so));
+  CounterSnapshot c = rt.counters();
+  CHECK(c.committed == 1);
+  CHECK(c.inline_executions == 0);
+  rt.wait(rt.submit(OpKind::Relu, {bi}, bo));
+  c = rt.counters();
+  CHECK(c.committed == 1);
+  CHECK(c.inline_executions == 1);
+  CHECK(read_all(rt, so) == std::vector<double>(4096, 0.0));
+  CHECK(read_all(rt, bo) == std::vector<double>(4097, 0.0));
+}
+
+TEST_CASE("attention context bound gates queue routing") {
+  RuntimeConfig cfg = small_config();
+  cfg.max_elements = 1u << 20;
+  Runtime rt(cfg);
+  std::mt19937_64 rng(303);
+  const int64_t h = 1, d = 8;
+  for (const int64_t t : {int64_t{2048}, int64_t{2049}}) {
+    auto q = rt.alloc_tensor(DType::F32, {h, d});
+    auto k = rt.alloc_tensor(DType::F32, {h, t, d});
+    auto v = rt.alloc_tensor(DType::F32, {h, t, d});
+    auto out = rt.alloc_tensor(DType::F32, {h, d});
+    fill(rt, q, random_vals(rng, static_cast<size_t>(h * d)));
+    fill(rt, k, random_vals(rng, static_cast<size_t>(h * t * d), -1.0, 1.0));
+    fill(rt, v, random_vals(rng, static_cast<size_t>(h * t * d), -1.0, 1.0));
+    const CounterSnapshot before = rt.counters();
+    REQUIRE(rt.wait(rt.submit(OpKind::Sdpa, {q, k, v}, out)) == TaskState::Done);
+    const CounterSnapshot after = rt.counters();
+    if (t <= 2048) CHECK(after.committed == before.committed + 1);
+    else CHECK(after.inline_executions == before.inline_executions + 1);
+  }
+}
+
+TEST_CASE("queue overflow falls back to inline execution without loss") {
+  Runtime rt(small_config(4, 1));
+  // hold the workers so the 4-slot ring fills (the reference pins its single
+  // worker with a gated host lambda, test_runtime.cpp:243-256)
+  check_abi(gpuos_dev_hold(rt.device(), 1), "hold");
+  constexpr int kTasks = 32;
+  std::vector<TensorView> outs;
+  std::vector<TaskHandle> hs;
+  for (int t = 0; t < kTasks; ++t) {
+    auto a = rt.alloc_tensor(DType::F32, {8});
+    auto b = rt.alloc_tensor(DType::F32, {8});
+    auto out = rt.alloc_tensor(DType::F32, {8});
+    fill(rt, a, std::vector<double>(8, t));
+    fill(rt, b, std::vector<double>(8, 100.0));
+    outs.push_back(out);
+    hs.push_back(rt.submit(OpKind::Add, {a, b}, out));
+  }
+  const CounterSnapshot mid = rt.counters();
+  REQUIRE(mid.queue_full_fallbacks > 0);
+  REQUIRE(mid.submitted == kTasks);
+  REQUIRE(mid.committed + mid.inline_executions == mid.submitted);
+  check_abi(gpuos_dev_hold(rt.device(), 0), "release");
+  rt.wait_all();
+  for (int t = 0; t < kTasks; ++t) {
+    REQUIRE(hs[static_cast<size_t>(t)].state() == TaskState::Done);
+    REQUIRE(read_all(rt, outs[static_cast<size_t>(t)]) == std::vector<double>(8, 100.0 + t));
+  }
+  const CounterSnapshot done = rt.counters();
+  CHECK(done.processed == done.committed);
+  CHECK(done.failed == 0);
+}
+
+TEST_CASE("injected operators: ids, exact values, cache, audit") {
+  Runtime rt(small_config());
+  const double p[2] = {2.0, -1.0};
+  const uint64_t id = rt.inject_operator("scale_add", p);
+  REQUIRE(id == kFirstInjectedId);
+  auto x = rt.alloc_tensor(DType::F32, {1});
+  auto y = rt.alloc_tensor(DType::F32, {1});
+  fill(rt, x, {1.5});
+  REQUIRE(rt.wait(rt.submit(id, {x}, y)) == TaskState::Done);
+  REQUIRE(read_all(rt, y)[0] == 2.0);
+  CHECK(rt.counters().committed == 1);
+  // same signature -> cache hit; different params -> new module and id
+  const uint64_t id2 = rt.inject_operator("scale_add", p);
+  CHECK(id2 == kFirstInjectedId + 1);
+  CHECK(rt.module_cache().compiles() == 1);
+  CHECK(rt.counters().cache_hits == 1);
+  const double q[2] = {3.0, 0.5};
+  const uint64_t id3 = rt.inject_operator("scale_add", q);
+  auto y3 = rt.alloc_tensor(DType::F32, {1});
+  REQUIRE(rt.wait(rt.submit(id3, {x}, y3)) == TaskState::Done);
+  CHECK(read_all(rt, y3)[0] == 5.0);
+  CHECK(rt.counters().injections == 3);
+  const auto audit = rt.table().audit();
+  REQUIRE(!audit.empty());
+  CHECK(audit.back().template_name == "scale_add");
+  CHECK(audit.back().version == rt.table().snapshot_version());
+  std::stringstream ss;
+  rt.table().export_audit_jsonl(ss);
+  const auto parsed = OperatorTable::parse_audit_jsonl(ss);
+  REQUIRE(parsed.size() == audit.size());
+  for (size_t i = 0; i < parsed.size(); ++i) {
+    CHECK(parsed[i].op_id == audit[i].op_id);
+    CHECK(parsed[i].signature == audit[i].signature);
+    CHECK(parsed[i].params == audit[i].params);
+    CHECK(parsed[i].version == audit[i].version);
+    CHECK(parsed[i].ts_ns == audit[i].ts_ns);
+  }
+  for (size_t i = 1; i < parsed.size(); ++i) CHECK(parsed[i].ts_ns > parsed[i - 1].ts_ns);
+}
+
+TEST_CASE("injected relu matches the builtin bit for bit, every template exact") {
+  Runtime rt(small_config());
+  rt.templates().add({"my_relu", "max(in0, 0)", 1});
+  const uint64_t id = rt.inject_operator("my_relu");
+  std::mt19937_64 rng(505);
+  const auto vals = random_vals(rng, 4096);
+  auto x = rt.alloc_tensor(DType::F32, {4096});
+  auto y1 = rt.alloc_tensor(DType::F32, {4096});
+  auto y2 = rt.alloc_tensor(DType::F32, {4096});
+  fill(rt, x, vals);
+  REQUIRE(rt.wait(rt.submit(OpKind::Relu, {x}, y1)) == TaskState::Done);
+  REQUIRE(rt.wait(rt.submit(id, {x}, y2)) == TaskState::Done);
+  REQUIRE(read_all(rt, y1) == read_all(rt, y2));
+  // every shipped template vs narrow_to(eval_expr) (test_opcompiler.cpp:528-558)
+  for (const std::string& name : rt.templates().names()) {
+    const OperatorTemplate t = rt.templates().get(name);
+    const double params[8] = {0.75, 2.5, 0, 0, 0, 0, 0, 0};
+    const uint64_t oid = rt.inject_operator(name, params);
+    std::vector<TensorView> ins;
+    std::vector<std::vector<double>> iv;
+    for (int i = 0; i < t.arity; ++i) {
+      ins.push_back(rt.alloc_tensor(DType::F64, {257}));
+      iv.push_back(random_vals(rng, 257, -3.0, 3.0));
+      fill(rt, ins.back(), iv.back());
+    }
+    auto out = rt.alloc_tensor(DType::F64, {257});
+    // module dtype F32 vs F64 output -> DTypeMismatch, then a F64 module
+    auto hm = rt.submit(oid, ins, out);
+    REQUIRE(rt.wait(hm) == TaskState::Failed);
+    CHECK(hm.error() == ErrorCode::DTypeMismatch);
+    const uint64_t oid64 = rt.inject_operator(name, params, DType::F64);
+    REQUIRE(rt.wait(rt.submit(oid64, ins, out)) == TaskState::Done);
+    const ExprPtr ast = parse_expression(t.source);
+    const auto got = read_all(rt, out);
+    for (size_t e = 0; e < 257; ++e) {
+      double in[4] = {0, 0, 0, 0};
+      for (int i = 0; i < t.arity; ++i) in[i] = iv[static_cast<size_t>(i)][e];
+      const double want = eval_expr(*ast, {in, 4}, {params, 8});
+      // + - * / sqrt abs max min are exact; exp/tanh allow 2 ulp of libdevice vs glibc
+      if (name == "sigmoid" || name == "silu" || name == "tanh_gate")
+        REQUIRE(close_tol(got[e], want, 4e-16));
+      else
+        REQUIRE((got[e] == want || (std::isnan(got[e]) && std::isnan(want))));
+    }
+  }
+}
+
+TEST_CASE("kill fails fast and re-injection revives the id") {
+  Runtime rt(small_config());
+  const double p[2] = {1.0, 0.0};
+  const uint64_t id = rt.inject_operator("scale_add", p);
+  auto x = rt.alloc_tensor(DType::F32, {16});
+  auto y = rt.alloc_tensor(DType::F32, {16});
+  REQUIRE(rt.wait(rt.submit(id, {x}, y)) == TaskState::Done);
+  const uint64_t v0 = rt.table().snapshot_version();
+  rt.kill_operator(static_cast<uint32_t>(id));
+  CHECK(rt.table().snapshot_version() == v0 + 1);
+  auto h = rt.submit(id, {x}, y);
+  REQUIRE(rt.wait(h) == TaskState::Failed);
+  REQUIRE(h.error() == ErrorCode::OperatorKilled);
+  // a killed builtin stays eligible and fails on the worker
+  rt.kill_operator(static_cast<uint32_t>(OpKind::Relu));
+  const uint64_t committed = rt.counters().committed;
+  auto h2 = rt.submit(OpKind::Relu, {x}, y);
+  REQUIRE(rt.wait(h2) == TaskState::Failed);
+  REQUIRE(h2.error() == ErrorCode::OperatorKilled);
+  CHECK(rt.counters().committed == committed + 1);
+  rt.inject_operator_at(static_cast<uint32_t>(id), "scale_add", p);
+  REQUIRE(rt.wait(rt.submit(id, {x}, y)) == TaskState::Done);
+  CHECK_THROWS_AS(rt.inject_operator_at(5, "scale_add", p), Error);
+  CHECK_THROWS_AS(rt.inject_operator_at(5000, "scale_add", p), Error);
+  CHECK_THROWS_AS(rt.inject_operator("no_such_template"), Error);
+}
+
+TEST_CASE("bad calls fail on the handle with the reference error codes") {
+  Runtime rt(small_config());
+  auto x = rt.alloc_tensor(DType::F32, {8});
+  auto y = rt.alloc_tensor(DType::F32, {8});
+  auto h1 = rt.submit(40, {x}, y);  // never injected: inline, NotInstalled
+  REQUIRE(rt.wait(h1) == TaskState::Failed);
+  REQUIRE(h1.error() == ErrorCode::NotInstalled);
+  auto h2 = rt.submit(uint64_t{1} << 33, {x}, y);
+  REQUIRE(rt.wait(h2) == TaskState::Failed);
+  REQUIRE(h2.error() == ErrorCode::OutOfRange);
+  TensorView bogus = x;
+  bogus.buffer = 999999;
+  auto h3 = rt.submit(OpKind::Relu, {bogus}, y);
+  REQUIRE(rt.wait(h3) == TaskState::Failed);
+  REQUIRE(h3.error() == ErrorCode::InvalidBuffer);
+  auto h4 = rt.submit(OpKind::Add, {x}, y);
+  REQUIRE(rt.wait(h4) == TaskState::Failed);
+  REQUIRE(h4.error() == ErrorCode::ArityError);
+  auto h5 = rt.submit(OpKind::Add, std::vector<TensorView>{x, x, x, x, x}, y);
+  REQUIRE(h5.error() == ErrorCode::ArityError);
+  auto xi = rt.alloc_tensor(DType::I32, {8});
+  auto h6 = rt.submit(OpKind::Gelu, {xi}, xi);
+  REQUIRE(rt.wait(h6) == TaskState::Failed);
+  REQUIRE(h6.error() == ErrorCode::DTypeMismatch);
+  auto e = rt.alloc_tensor(DType::F32, {3, 0});
+  auto eo = rt.alloc_tensor(DType::F32, {3});
+  auto h7 = rt.submit(OpKind::ReduceMax, {e}, eo);
+  REQUIRE(rt.wait(h7) == TaskState::Failed);
+  REQUIRE(h7.error() == ErrorCode::EmptyAxis);
+  REQUIRE(rt.worker_alive());
+  REQUIRE(rt.wait(rt.submit(OpKind::Relu, {x}, y)) == TaskState::Done);
+  TaskHandle invalid;
+  CHECK_FALSE(invalid.valid());
+  CHECK_THROWS_AS(invalid.state(), Error);
+}
+
+TEST_CASE("queue and inline paths agree bit for bit") {
+  RuntimeConfig qc = small_config();
+  RuntimeConfig ic = small_config();
+  ic.max_elements = 0;  // everything inline
+  Runtime rq(qc), ri(ic);
+  std::mt19937_64 rng(707);
+  auto run_both = [&](OpKind k, const std::vector<std::vector<int64_t>>& in_shapes, const std::vector<int64_t>& out_shape,
+                      std::vector<double> scalars, DType dt) {
+    std::vector<std::vector<double>> vals;
+    std::vector<TensorView> iq, ii;
+    for (const auto& s : in_shapes) {
+      iq.push_back(rq.alloc_tensor(dt, Shape(s)));
+      ii.push_back(ri.alloc_tensor(dt, Shape(s)));
+      vals.push_back(random_vals(rng, static_cast<size_t>(iq.back().numel()), -2.0, 2.0));
+      fill(rq, iq.back(), vals.back());
+      fill(ri, ii.back(), vals.back());
+    }
+    auto oq = rq.alloc_tensor(dt, Shape(out_shape));
+    auto oi = ri.alloc_tensor(dt, Shape(out_shape));
+    REQUIRE(rq.wait(rq.submit(static_cast<uint64_t>(k), iq, oq, scalars)) == TaskState::Done);
+    REQUIRE(ri.wait(ri.submit(static_cast<uint64_t>(k), ii, oi, scalars)) == TaskState::Done);
+    REQUIRE(read_all(rq, oq) == read_all(ri, oi));
+  };
+  run_both(OpKind::Add, {{64, 33}, {1, 33}}, {64, 33}, {}, DType::F32);
+  run_both(OpKind::Gelu, {{1000}}, {1000}, {}, DType::F32);
+  run_both(OpKind::Softmax, {{16, 128}}, {16, 128}, {}, DType::F32);
+  run_both(OpKind::LayerNorm, {{8, 96}, {96}, {96}}, {8, 96}, {1e-5}, DType::F64);
+  run_both(OpKind::ReduceSum, {{32, 1500}}, {32}, {}, DType::F32);
+  run_both(OpKind::Rope, {{6, 64}, {6}}, {6, 64}, {}, DType::F64);
+  run_both(OpKind::Sdpa, {{4, 64}, {4, 300, 64}, {4, 300, 64}}, {4, 64}, {}, DType::F32);
+  run_both(OpKind::Mul, {{3000}, {3000}}, {3000}, {}, DType::BF16);
+  CHECK(ri.counters().committed == 0);
+}
+
+TEST_CASE("accounting identity holds at quiescence") {
+  Runtime rt(small_config(64, 4));
+  auto x = rt.alloc_tensor(DType::F32, {4096});
+  auto y = rt.alloc_tensor(DType::F32, {4096});
+  auto big = rt.alloc_tensor(DType::F32, {70000});
+  for (int i = 0; i < 500; ++i) {
+    rt.submit(OpKind::Relu, {x}, y);
+    if (i % 50 == 0) rt.submit(OpKind::Relu, {big}, big);
+  }
+  rt.submit(OpKind::Add, {x}, y);  // fails on the worker
+  rt.wait_all();
+  const CounterSnapshot c = rt.counters();
+  CHECK(c.submitted == c.inline_executions + c.committed + rt.fusion_absorbed());
+  CHECK(c.processed == c.committed);
+  CHECK(c.failed == 1);
+  const auto s = rt.peek_queue();
+  CHECK(s.processed == s.head);
+  CHECK(s.head == s.tail);
+}
+
+TEST_CASE("hot swap under load: every row is entirely one variant, no canary hits") {
+  Runtime rt(small_config(4096, 0));
+  const double pa[2] = {1.5, -0.25};
+  const double pb[2] = {-2.0, 3.0};
+  const uint32_t id = static_cast<uint32_t>(rt.inject_operator("scale_add", pa));
+  constexpr int kRows = 8, kN = 4096, kTasks = 20000;
+  std::vector<TensorView> ins, outs;
+  std::mt19937_64 rng(808);
+  std::vector<std::vector<double>> iv;
+  for (int r = 0; r < kRows; ++r) {
+    ins.push_back(rt.alloc_tensor(DType::F32, {kN}));
+    iv.push_back(random_vals(rng, kN, -1.0, 1.0));
+    fill(rt, ins.back(), iv.back());
+  }
+  for (int t = 0; t < kTasks; ++t) outs.push_back(rt.alloc_tensor(DType::F32, {kN}));
+  std::vector<TaskHandle> hs;
+  hs.reserve(kTasks);
+  for (int t = 0; t < kTasks; ++t) {
+    hs.push_back(rt.submit(id, {ins[static_cast<size_t>(t % kRows)]}, outs[static_cast<size_t>(t)]));
+    if (t == kTasks / 2) rt.inject_operator_at(id, "scale_add", pb);
+  }
+  rt.wait_all();
+  int old_rows = 0, new_rows = 0;
+  for (int t = 0; t < kTasks; ++t) {
+    REQUIRE(hs[static_cast<size_t>(t)].state() == TaskState::Done);
+    const auto got = read_all(rt, outs[static_cast<size_t>(t)]);
+    const auto& x = iv[static_cast<size_t>(t % kRows)];
+    bool all_a = true, all_b = true;
+    for (int e = 0; e < kN; ++e) {
+      const double xv = f32(x[static_cast<size_t>(e)]);
+      all_a = all_a && got[static_cast<size_t>(e)] == f32(xv * 1.5 + -0.25);
+      all_b = all_b && got[static_cast<size_t>(e)] == f32(xv * -2.0 + 3.0);
+    }
+    REQUIRE((all_a || all_b));
+    (all_a ? old_rows : new_rows) += 1;
+    if (t > kTasks / 2 + 2 * 4096) CHECK(all_b);  // past the ring's in-flight window
+  }
+  CHECK(old_rows > 0);
+  CHECK(new_rows > 0);
+  CHECK(rt.canary_hits() == 0);
+  const gpuos_inject_stats& st = rt.last_inject_stats();
+  std::printf("  swap: upload %.1f us, epoch wait %.1f us, bank write %.1f us, flip %.1f us; rows old=%d new=%d\n",
+              st.upload_ns / 1e3, st.epoch_wait_ns / 1e3, st.bank_write_ns / 1e3, st.flip_ns / 1e3, old_rows, new_rows);
+}
+
+TEST_CASE("shutdown drains every committed task") {
+  Runtime rt(small_config(1024, 0));
+  auto x = rt.alloc_tensor(DType::F32, {256});
+  auto y = rt.alloc_tensor(DType::F32, {256});
+  std::vector<TaskHandle> hs;
+  for (int i = 0; i < 10000; ++i) hs.push_back(rt.submit(OpKind::Relu, {x}, y));
+  rt.shutdown();
+  for (const TaskHandle& h : hs) REQUIRE(h.state() == TaskState::Done);
+  REQUIRE_FALSE(rt.worker_alive());
+}
+
+TEST_CASE("kv_append writes the row and reports CacheFull past capacity") {
+  Runtime rt(small_config());
+  const int64_t h = 2, cap = 4, d = 8;
+  auto kc = rt.alloc_tensor(DType::F32, {h, cap, d});
+  auto vc = rt.alloc_tensor(DType::F32, {h, cap, d});
+  auto nk = rt.alloc_tensor(DType::F32, {h, d});
+  auto nv = rt.alloc_tensor(DType::F32, {h, d});
+  std::mt19937_64 rng(909);
+  const auto wk = random_vals(rng, static_cast<size_t>(h * d)), wv = random_vals(rng, static_cast<size_t>(h * d));
+  fill(rt, nk, wk);
+  fill(rt, nv, wv);
+  for (int64_t cur = 0; cur < cap; ++cur)
+    REQUIRE(rt.wait(rt.submit(OpKind::KvAppend, {nk, nv, vc}, kc, {static_cast<double>(cur)})) == TaskState::Done);
+  BoundView bk(rt.pool(), kc), bv(rt.pool(), vc);
+  for (int64_t hh = 0; hh < h; ++hh)
+    for (int64_t cur = 0; cur < cap; ++cur)
+      for (int64_t e = 0; e < d; ++e) {
+        REQUIRE(bk.load((hh * cap + cur) * d + e) == f32(wk[static_cast<size_t>(hh * d + e)]));
+        REQUIRE(bv.load((hh * cap + cur) * d + e) == f32(wv[static_cast<size_t>(hh * d + e)]));
+      }
+  auto bad = rt.submit(OpKind::KvAppend, {nk, nv, vc}, kc, {static_cast<double>(cap)});
+  REQUIRE(rt.wait(bad) == TaskState::Failed);
+  REQUIRE(bad.error() == ErrorCode::CacheFull);
+}
+
+TEST_CASE("telemetry: tracepoints per dispatch, CSV and JSONL round trip") {
+  Runtime rt(small_config());
+  auto x = rt.alloc_tensor(DType::F32, {64});
+  auto y = rt.alloc_tensor(DType::F32, {64});
+  for (int i = 0; i < 100; ++i) rt.submit(OpKind::Relu, {x}, y);
+  rt.wait_all();
+  const auto tr = rt.trace();
+  REQUIRE(tr.size() == 100);
+  for (const Tracepoint& t : tr) {
+    CHECK(t.dequeue_ns >= t.enqueue_ns);
+    CHECK(t.exec_ns >= 1);
+    CHECK(t.op_id == static_cast<uint64_t>(OpKind::Relu));
+  }
+  std::stringstream cs, js;
+  export_csv(tr, cs);
+  export_jsonl(tr, js);
+  CHECK(parse_trace_csv(cs) == tr);
+  CHECK(parse_trace_jsonl(js) == tr);
+  const auto lat = latency_ns(tr);
+  std::printf("  queue latency p50 %llu ns p99 %llu ns\n", (unsigned long long)percentile(lat, 0.5),
+              (unsigned long long)percentile(lat, 0.99));
+}
