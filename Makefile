@@ -21,7 +21,7 @@ all: lib bench cpp-tests oracle
 
 lib: $(LIBDIR)/libgpuos_cuda.so
 bench: $(LIBDIR)/libgpuos_bench.so
-cpp-tests: build/cpp/test_runtime
+cpp-tests: build/cpp/test_runtime build/cpp/test_host
 
 $(OBJ)/worker.o: $(CSRC)/worker.cu $(DEV_HDRS)
 	@mkdir -p $(OBJ)
@@ -33,7 +33,7 @@ $(OBJ)/capi.o: $(CSRC)/capi.cu $(DEV_HDRS)
 
 $(LIBDIR)/libgpuos_cuda.so: $(OBJ)/worker.o $(OBJ)/capi.o
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lnvrtc -lnvJitLink
+	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 $(LIBDIR)/libgpuos_bench.so: tools/bench/gpuos_bench.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN'
@@ -50,3 +50,7 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib bench cpp-tests oracle clean
+
+build/cpp/test_host: tests/cpp/test_host.cpp tests/cpp/check.hpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	@mkdir -p build/cpp
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread

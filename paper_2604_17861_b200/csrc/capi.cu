@@ -1087,57 +1087,133 @@ int gpuos_copy_async(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, i
 }
 
 // ---------------------------------------------------------------- NVRTC / nvJitLink
+// Loaded on first use with dlopen(RTLD_LOCAL) from the CUDA toolkit this
+// library was built against, so a different libnvJitLink/libnvrtc already in
+// the process (e.g. one bundled with PyTorch) cannot shadow the 12.9 symbols.
+}  // extern "C"
+#include <dlfcn.h>
+namespace {
+struct JitApi {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*log)(nvrtcProgram, char*);
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*cubin)(nvrtcProgram, char*);
+  nvrtcResult (*destroy)(nvrtcProgram*);
+  nvJitLinkResult (*l_create)(nvJitLinkHandle*, uint32_t, const char**);
+  nvJitLinkResult (*l_add)(nvJitLinkHandle, nvJitLinkInputType, const void*, size_t, const char*);
+  nvJitLinkResult (*l_complete)(nvJitLinkHandle);
+  nvJitLinkResult (*l_err_size)(nvJitLinkHandle, size_t*);
+  nvJitLinkResult (*l_err)(nvJitLinkHandle, char*);
+  nvJitLinkResult (*l_cubin_size)(nvJitLinkHandle, size_t*);
+  nvJitLinkResult (*l_cubin)(nvJitLinkHandle, void*);
+  nvJitLinkResult (*l_destroy)(nvJitLinkHandle*);
+};
+
+void* open_first(const char* const* names) {
+  for (const char* const* n = names; *n; ++n)
+    if (void* h = dlopen(*n, RTLD_NOW | RTLD_LOCAL)) return h;
+  return nullptr;
+}
+
+JitApi load_jit() {
+  JitApi a;
+  static const char* rtc[] = {"/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12", nullptr};
+  static const char* lnk[] = {"/usr/local/cuda/lib64/libnvJitLink.so.12", "libnvJitLink.so.12", nullptr};
+  void* hr = open_first(rtc);
+  void* hl = open_first(lnk);
+  if (!hr || !hl) {
+    a.why = "cannot load libnvrtc/libnvJitLink";
+    return a;
+  }
+#define GPUOS_SYM(h, field, name)                       \
+  a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name)); \
+  if (!a.field) {                                       \
+    a.why = std::string("missing symbol ") + name;      \
+    return a;                                           \
+  }
+  GPUOS_SYM(hr, create, "nvrtcCreateProgram");
+  GPUOS_SYM(hr, compile, "nvrtcCompileProgram");
+  GPUOS_SYM(hr, log_size, "nvrtcGetProgramLogSize");
+  GPUOS_SYM(hr, log, "nvrtcGetProgramLog");
+  GPUOS_SYM(hr, cubin_size, "nvrtcGetCUBINSize");
+  GPUOS_SYM(hr, cubin, "nvrtcGetCUBIN");
+  GPUOS_SYM(hr, destroy, "nvrtcDestroyProgram");
+  GPUOS_SYM(hl, l_create, "__nvJitLinkCreate_12_9");
+  GPUOS_SYM(hl, l_add, "__nvJitLinkAddData_12_9");
+  GPUOS_SYM(hl, l_complete, "__nvJitLinkComplete_12_9");
+  GPUOS_SYM(hl, l_err_size, "__nvJitLinkGetErrorLogSize_12_9");
+  GPUOS_SYM(hl, l_err, "__nvJitLinkGetErrorLog_12_9");
+  GPUOS_SYM(hl, l_cubin_size, "__nvJitLinkGetLinkedCubinSize_12_9");
+  GPUOS_SYM(hl, l_cubin, "__nvJitLinkGetLinkedCubin_12_9");
+  GPUOS_SYM(hl, l_destroy, "__nvJitLinkDestroy_12_9");
+#undef GPUOS_SYM
+  a.ok = true;
+  return a;
+}
+
+const JitApi& jit_api() {
+  static const JitApi api = load_jit();
+  return api;
+}
+}  // namespace
+extern "C" {
 
 int gpuos_jit_compile(const char* src, const char* const* opts, int nopts, void** cubin, size_t* size,
                       uint64_t* compile_ns, uint64_t* link_ns, char* log, size_t logcap) {
   if (!src || !cubin || !size) return GPUOS_INTERNAL;
   auto put_log = [&](const std::string& s) {
-    if (log && logcap) {
-      std::snprintf(log, logcap, "%s", s.c_str());
-    }
+    if (log && logcap) std::snprintf(log, logcap, "%s", s.c_str());
   };
+  const JitApi& J = jit_api();
+  if (!J.ok) {
+    put_log(J.why);
+    return GPUOS_INTERNAL;
+  }
   const uint64_t t0 = steady_ns();
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src, "gpuos_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return GPUOS_INTERNAL;
+  if (J.create(&prog, src, "gpuos_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return GPUOS_INTERNAL;
   std::vector<const char*> o;
   o.push_back("-arch=sm_100a");
   o.push_back("-rdc=true");
   o.push_back("--fmad=false");
   for (int i = 0; i < nopts; ++i) o.push_back(opts[i]);
-  const nvrtcResult r = nvrtcCompileProgram(prog, (int)o.size(), o.data());
-  if (r != NVRTC_SUCCESS) {
+  if (J.compile(prog, (int)o.size(), o.data()) != NVRTC_SUCCESS) {
     size_t n = 0;
-    nvrtcGetProgramLogSize(prog, &n);
+    J.log_size(prog, &n);
     std::string l(n, '\0');
-    nvrtcGetProgramLog(prog, l.data());
+    J.log(prog, l.data());
     put_log(l);
-    nvrtcDestroyProgram(&prog);
+    J.destroy(&prog);
     return GPUOS_SYNTAX_ERROR;
   }
   size_t n = 0;
-  nvrtcGetCUBINSize(prog, &n);
+  J.cubin_size(prog, &n);
   std::vector<char> relo(n);
-  nvrtcGetCUBIN(prog, relo.data());
-  nvrtcDestroyProgram(&prog);
+  J.cubin(prog, relo.data());
+  J.destroy(&prog);
   const uint64_t t1 = steady_ns();
   nvJitLinkHandle h;
   const char* lopts[] = {"-arch=sm_100a"};
-  if (nvJitLinkCreate(&h, 1, lopts) != NVJITLINK_SUCCESS) return GPUOS_INTERNAL;
-  if (nvJitLinkAddData(h, NVJITLINK_INPUT_CUBIN, relo.data(), relo.size(), "gpuos_jit") != NVJITLINK_SUCCESS ||
-      nvJitLinkComplete(h) != NVJITLINK_SUCCESS) {
+  if (J.l_create(&h, 1, lopts) != NVJITLINK_SUCCESS) return GPUOS_INTERNAL;
+  if (J.l_add(h, NVJITLINK_INPUT_CUBIN, relo.data(), relo.size(), "gpuos_jit") != NVJITLINK_SUCCESS ||
+      J.l_complete(h) != NVJITLINK_SUCCESS) {
     size_t ln = 0;
-    nvJitLinkGetErrorLogSize(h, &ln);
+    J.l_err_size(h, &ln);
     std::string l(ln, '\0');
-    nvJitLinkGetErrorLog(h, l.data());
+    J.l_err(h, l.data());
     put_log(l);
-    nvJitLinkDestroy(&h);
+    J.l_destroy(&h);
     return GPUOS_VERIFY_ERROR;
   }
   size_t cs = 0;
-  nvJitLinkGetLinkedCubinSize(h, &cs);
+  J.l_cubin_size(h, &cs);
   void* out = std::malloc(cs);
-  nvJitLinkGetLinkedCubin(h, out);
-  nvJitLinkDestroy(&h);
+  J.l_cubin(h, out);
+  J.l_destroy(&h);
   const uint64_t t2 = steady_ns();
   *cubin = out;
   *size = cs;
