@@ -54,3 +54,10 @@ clean:
 build/cpp/test_host: tests/cpp/test_host.cpp tests/cpp/check.hpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	@mkdir -p build/cpp
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
+
+# GPU-box probes (producer cost breakdown, finite worker generation for ncu)
+probes: build/probe/submit_cost build/probe/profile_worker
+build/probe/%: tools/probe/%.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	@mkdir -p build/probe
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
+.PHONY: probes

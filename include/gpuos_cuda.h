@@ -232,6 +232,11 @@ int gpuos_dev_sm_count(gpuos_dev* dev, uint32_t* n);
 /* Hold (1) / release (0) ticket claims: idle workers stop claiming while held,
  * so published work stays queued (lets tests fill the ring; stop releases). */
 int gpuos_dev_hold(gpuos_dev* dev, int hold);
+/* With the workers stopped: publish the shutdown sentinel behind all queued
+ * work, run one worker generation until it drains the ring and exits, and
+ * report its duration (CUDA events on the worker stream).  A finite kernel
+ * for ncu and for device-capacity measurements. */
+int gpuos_dev_run_finite(gpuos_dev* dev, float* kernel_ms);
 /* Live yield cadence (executor.hpp:107). */
 int gpuos_set_yield_every(gpuos_dev* dev, uint64_t n);
 /* Convert a device %globaltimer stamp to host steady_clock ns. */

@@ -98,7 +98,7 @@ assert C.sizeof(View) == 48 and C.sizeof(Task) == SLOT_BYTES and C.sizeof(Instr)
 EXPORTS = [
     "gpuos_abi_version", "gpuos_default_cfg", "gpuos_dev_open", "gpuos_dev_close", "gpuos_dev_alive",
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
-    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
+    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
     "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
     "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
@@ -134,6 +134,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_dev_sm_count": ([P, C.POINTER(U32)], I),
         "gpuos_set_yield_every": ([P, U64], I),
         "gpuos_dev_hold": ([P, I], I),
+        "gpuos_dev_run_finite": ([P, C.POINTER(C.c_float)], I),
         "gpuos_dev_clock_offset": ([P, C.POINTER(C.c_int64)], I),
         "gpuos_buf_alloc": ([P, I, U64, C.POINTER(U64), C.POINTER(P)], I),
         "gpuos_buf_free": ([P, U64], I),

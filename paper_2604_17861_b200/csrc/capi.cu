@@ -73,7 +73,7 @@ struct gpuos_dev {
   std::atomic<uint64_t> published{0};
   uint32_t workers = 0, threads = 0, smem = 0;
   std::atomic<bool> running{false};
-  uint64_t last_sentinel = 0;
+  uint64_t resume_pos = 0;  // first ticket of the next worker generation
   // table
   std::mutex table_mu;
   std::vector<TableEntry> bank[2];
@@ -158,13 +158,6 @@ static int dev_write_field(gpuos_dev* d, size_t off, const void* src, size_t n) 
   return GPUOS_OK;
 }
 
-static uint64_t slot_checksum(const uint64_t* w) {
-  uint64_t h = 0;
-  for (uint32_t i = 0; i < GPUOS_SLOT_BYTES / 8; ++i)
-    if (i != 7) h += gdev::slot_mix(w[i], i);
-  return h;
-}
-
 extern "C" {
 
 int gpuos_abi_version(void) { return GPUOS_ABI_VERSION; }
@@ -226,7 +219,7 @@ static uint64_t tsc_to_ns(const gpuos_dev* d, uint64_t tsc) {
 }
 
 static int launch_workers(gpuos_dev* d) {
-  GPUOS_CK(gdev::launch_worker(d->S, d->workers, d->threads, d->smem, d->ks));
+  GPUOS_CK(gdev::launch_worker(d->S, d->workers, gdev::worker_threads(), d->smem, d->ks));
   note_resident(d->device, +1);
   d->running.store(true, std::memory_order_release);
   return GPUOS_OK;
@@ -242,7 +235,7 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   if (cfg.table_slots == 0) return GPUOS_ZERO_SLOTS;  // optable.hpp:101
   if (cfg.table_slots < GPUOS_FIRST_INJECTED_ID + 1) cfg.table_slots = GPUOS_FIRST_INJECTED_ID + 1;
   if (cfg.threads_per_worker == 0) cfg.threads_per_worker = 256;
-  if (cfg.threads_per_worker != 256) return GPUOS_OUT_OF_RANGE;  // worker kernel is built for 256
+  if (cfg.threads_per_worker != 256) return GPUOS_OUT_OF_RANGE;  // executor group is built for 256 (+1 fetch warp)
   if (cfg.trace_capacity == 0) cfg.trace_capacity = 1;
   if (cfg.backoff_max_exp > 10) cfg.backoff_max_exp = 10;
 
@@ -265,7 +258,16 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
 
   d->threads = cfg.threads_per_worker;
   d->smem = gdev::worker_smem_bytes();
+  // default: one worker CTA per SM.  A second CTA per SM
+  // would fit (288 threads, <=112 registers, 96 KB shared), but then the
+  // conventional path's standalone kernels and the runtime's memsets could
+  // not be scheduled next to a resident generation; num_workers can still
+  // ask for up to worker_occupancy() per SM.
+  int per_sm = 0;
+  GPUOS_CK(gdev::worker_occupancy(&per_sm));
+  if (per_sm < 1) per_sm = 1;
   d->workers = cfg.num_workers ? cfg.num_workers : d->sms;
+  if (d->workers > d->sms * (uint32_t)per_sm) d->workers = d->sms * (uint32_t)per_sm;
   if (d->workers > gdev::kMaxWorkers) d->workers = gdev::kMaxWorkers;
 
   // ring capacity: power of two, min 2 (queue.hpp:164-165)
@@ -343,8 +345,14 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
 
   int rc = calibrate_clocks(d.get());
   if (rc) return rc;
-  rc = launch_workers(d.get());
-  if (rc) return rc;
+  // GPUOS_DEFER_START=1: no resident generation until gpuos_dev_start /
+  // gpuos_dev_run_finite (profilers serialise launches, so a persistent
+  // generation launched here would never return under ncu).
+  const char* defer = std::getenv("GPUOS_DEFER_START");
+  if (!(defer && defer[0] == '1')) {
+    rc = launch_workers(d.get());
+    if (rc) return rc;
+  }
   *out = d.release();
   return GPUOS_OK;
 }
@@ -364,7 +372,7 @@ int gpuos_dev_stop(gpuos_dev* d) {
   std::memset(&t, 0, sizeof(t));
   t.flags = GPUOS_FLAG_SHUTDOWN;
   gpuos_ring_publish(d, pos, &t);
-  d->last_sentinel = pos;
+  d->resume_pos = pos + 1;
   GPUOS_CK(cudaSetDevice(d->device));
   GPUOS_CK(cudaStreamSynchronize(d->ks));
   d->running.store(false, std::memory_order_release);
@@ -377,7 +385,7 @@ int gpuos_dev_start(gpuos_dev* d) {
   if (d->running.load(std::memory_order_acquire)) return GPUOS_ALREADY_STARTED;
   GPUOS_CK(cudaSetDevice(d->device));
   // resume right after the consumed sentinel: tickets past it were abandoned
-  const uint64_t next = d->last_sentinel + 1;
+  const uint64_t next = d->resume_pos;
   DevState& s = d->shadow;
   s.claim = next;
   s.hint = next;
@@ -387,6 +395,44 @@ int gpuos_dev_start(gpuos_dev* d) {
   if (!rc) rc = dev_write_field(d, offsetof(DevState, stop_pos), &s.stop_pos, 8);
   if (rc) return rc;
   return launch_workers(d);
+}
+
+// Finite generation (profiling, device-capacity runs): the sentinel goes
+// behind everything already published, then one worker generation drains the
+// ring and exits.  Under ncu the launch is a plain finite kernel.
+int gpuos_dev_run_finite(gpuos_dev* d, float* kernel_ms) {
+  if (!d) return GPUOS_INTERNAL;
+  if (d->running.load(std::memory_order_acquire)) return GPUOS_ALREADY_STARTED;
+  GPUOS_CK(cudaSetDevice(d->device));
+  const uint64_t next = d->resume_pos;
+  uint64_t pos = 0;
+  if (gpuos_ring_reserve(d, &pos) != GPUOS_OK) return GPUOS_QUEUE_FULL;
+  gpuos_task t;
+  std::memset(&t, 0, sizeof(t));
+  t.flags = GPUOS_FLAG_SHUTDOWN;
+  gpuos_ring_publish(d, pos, &t);
+  DevState& s = d->shadow;
+  s.claim = next;
+  s.hint = pos + 1;
+  s.stop_pos = gdev::kRunning;
+  int rc = dev_write_field(d, offsetof(DevState, claim), &s.claim, 8);
+  if (!rc) rc = dev_write_field(d, offsetof(DevState, hint), &s.hint, 8);
+  if (!rc) rc = dev_write_field(d, offsetof(DevState, stop_pos), &s.stop_pos, 8);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  GPUOS_CK(cudaEventCreate(&e0));
+  GPUOS_CK(cudaEventCreate(&e1));
+  GPUOS_CK(cudaEventRecord(e0, d->ks));
+  GPUOS_CK(gdev::launch_worker(d->S, d->workers, gdev::worker_threads(), d->smem, d->ks));
+  GPUOS_CK(cudaEventRecord(e1, d->ks));
+  GPUOS_CK(cudaStreamSynchronize(d->ks));
+  float ms = 0;
+  GPUOS_CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (kernel_ms) *kernel_ms = ms;
+  d->resume_pos = pos + 1;
+  return GPUOS_OK;
 }
 
 int gpuos_dev_close(gpuos_dev* d) {
@@ -446,6 +492,16 @@ int gpuos_dev_clock_offset(gpuos_dev* d, int64_t* off) {
 
 // ---------------------------------------------------------------- buffers
 
+// GPUOS_DEVICE_BUFFERS=1 (experiments): plain cudaMalloc storage instead of
+// managed memory; host pointers from BufferPool then are not dereferenceable.
+static bool device_only_buffers() {
+  static const bool on = [] {
+    const char* e = std::getenv("GPUOS_DEVICE_BUFFERS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int gpuos_buf_alloc(gpuos_dev* d, int dtype, uint64_t n, uint64_t* id, void** ptr) {
   if (!d || !id) return GPUOS_INTERNAL;
   if (dtype < 0 || dtype > GPUOS_BF16) return GPUOS_DTYPE_MISMATCH;
@@ -459,12 +515,12 @@ int gpuos_buf_alloc(gpuos_dev* d, int dtype, uint64_t n, uint64_t* id, void** pt
     p = fl->second.back();
     fl->second.pop_back();
   } else if (bytes > kArenaChunk / 4) {
-    GPUOS_CK(cudaMallocManaged(&p, bytes));
+    GPUOS_CK(device_only_buffers() ? cudaMalloc(&p, bytes) : cudaMallocManaged(&p, bytes));
     d->managed_blocks.push_back(p);
   } else {
     if (d->arena_left < bytes) {
       void* blk = nullptr;
-      GPUOS_CK(cudaMallocManaged(&blk, kArenaChunk));
+      GPUOS_CK(device_only_buffers() ? cudaMalloc(&blk, kArenaChunk) : cudaMallocManaged(&blk, kArenaChunk));
       d->managed_blocks.push_back(blk);
       d->arena_cur = (char*)blk;
       d->arena_left = kArenaChunk;
@@ -524,6 +580,7 @@ int gpuos_buf_copy(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int
 
 int gpuos_buf_prefetch(gpuos_dev* d, uint64_t id) {
   if (!d) return GPUOS_INTERNAL;
+  if (device_only_buffers()) return GPUOS_OK;  // already device memory
   void* p = nullptr;
   uint64_t bytes = 0;
   {
@@ -612,30 +669,37 @@ int gpuos_ring_reserve(gpuos_dev* d, uint64_t* pos) {
   if (__atomic_load_n(w, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
   d->reserve = p + 1;
   *pos = p;
-  // the device freed upcoming slots over PCIe: pull their sequence words in early
-  _mm_prefetch(d->ring + ((p + 16) & d->mask) * GPUOS_SLOT_BYTES, _MM_HINT_T0);
+  // The device freed upcoming slots over PCIe, which invalidated their first
+  // line in the host caches: fetch it for writing well ahead of use.
+  const char* ahead = d->ring + ((p + 16) & d->mask) * GPUOS_SLOT_BYTES;
+  asm volatile("prefetchw (%0)" ::"r"(ahead));
   return GPUOS_OK;
 }
 
+// Ordinary write-back stores, publication word last.  x86 stores become
+// visible in program order (TSO), also to the device's coherent PCIe reads,
+// so a reader that sees word 0 == pos+1 sees a payload at least that new;
+// a warp-wide read can still interleave with the writes chunk by chunk,
+// which the checksum catches (the device re-reads).  No fence: an sfence
+// per slot (streaming stores) measured ~200 ns, profiles/r01_ring_store.log.
 int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
-  alignas(64) uint64_t w[GPUOS_SLOT_BYTES / 8];
-  std::memcpy(w, task, GPUOS_SLOT_BYTES);
-  w[0] = pos + 1;
-  if (d->shadow.trace_on) w[5] = __rdtsc();  // enqueue stamp, converted at trace export
-  w[7] = 0;
-  w[7] = slot_checksum(w);
-  char* dst = d->ring + (pos & d->mask) * GPUOS_SLOT_BYTES;
-  // Streaming stores for the whole slot and the tail: these lines were last
-  // touched by the device (slot free, tail polls), so ordinary stores would
-  // each pay a read-for-ownership.  One sfence makes them globally visible;
-  // a reader that catches the slot half-written fails the checksum and
-  // re-reads, and a tail seen early only wakes a poller one read too soon.
-  for (int i = 1; i < GPUOS_SLOT_BYTES / 16; ++i)
-    _mm_stream_si128((__m128i*)(dst + 16 * i), _mm_load_si128((const __m128i*)((const char*)w + 16 * i)));
-  _mm_stream_si64((long long*)(dst + 8), (long long)w[1]);
-  _mm_stream_si64((long long*)dst, (long long)w[0]);
-  _mm_stream_si64((long long*)d->tail, (long long)(pos + 1));
-  _mm_sfence();
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(task);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (pos & d->mask) * GPUOS_SLOT_BYTES);
+  uint64_t h = gdev::slot_term(pos + 1, 0);
+  for (uint32_t i = 1; i < 7; ++i) {
+    uint64_t v = src[i];
+    if (i == 5 && d->shadow.trace_on) v = __rdtsc();  // enqueue stamp, converted at trace export
+    dst[i] = v;
+    h += gdev::slot_term(v, i);
+  }
+  for (uint32_t i = 8; i < GPUOS_SLOT_BYTES / 8; ++i) {
+    const uint64_t v = src[i];
+    dst[i] = v;
+    h += gdev::slot_term(v, i);
+  }
+  dst[7] = h;
+  __atomic_store_n(&dst[0], pos + 1, __ATOMIC_RELEASE);
+  __atomic_store_n(d->tail, pos + 1, __ATOMIC_RELEASE);
   d->published.store(pos + 1, std::memory_order_relaxed);
   return GPUOS_OK;
 }

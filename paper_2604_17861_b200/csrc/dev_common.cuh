@@ -91,14 +91,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// Word mixer for the slot checksum; the host computes the same function
-// (capi.cu) over the 48 words of a slot with word 7 (the checksum) as 0.
-__host__ __device__ __forceinline__ uint64_t slot_mix(uint64_t w, uint32_t i) {
-  uint64_t x = w + (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull;
-  x ^= x >> 31;
-  x *= 0xBF58476D1CE4E5B9ull;
-  x ^= x >> 29;
-  return x;
+// Slot checksum term: word i weighted by the odd constant 2i+1 (mod 2^64).
+// The host sums it over the 48 words of a slot with word 7 (the checksum)
+// left out; the device recomputes the sum warp-wide.  A stale 16-byte chunk
+// from the slot's previous lap changes the sum unless its difference is 0,
+// so torn reads (queue.hpp:249-251) are caught at ~1 multiply-add per word.
+__host__ __device__ __forceinline__ uint64_t slot_term(uint64_t w, uint32_t i) {
+  return w * (uint64_t)(2 * i + 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -16,8 +16,8 @@ constexpr uint64_t kRunning = ~0ull;    // stop_pos while running
 constexpr uint32_t kNumKinds = 80;      // module jump-table slots
 constexpr uint32_t kTaskBytes = 384;
 constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
-constexpr uint32_t kHeaderBytes = 1024;  // worker: 2 task buffers + 2 control blocks + counters
-constexpr uint32_t kScratchBytes = 96 * 1024;
+constexpr uint32_t kHeaderBytes = 4096;  // worker: task buffers, control blocks, counters, entry cache
+constexpr uint32_t kScratchBytes = 92 * 1024;
 constexpr uint32_t kLaunchCounters = 1u << 16;
 
 // One operator-table entry (optable.hpp:40-48): the device function is named
@@ -103,5 +103,7 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
                         uint32_t* counter, cudaStream_t st);
 cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st);
 uint32_t worker_smem_bytes();
+uint32_t worker_threads();
+cudaError_t worker_occupancy(int* per_sm);
 
 }  // namespace gdev

@@ -67,6 +67,66 @@ struct SharedCtl {
 constexpr uint32_t kCtlStride = 112;
 static_assert(sizeof(SharedCtl) <= kCtlStride, "SharedCtl must fit its stride");
 
+// Worker CTA shape: warp 0 fetches, warps 1..8 execute (one 256-thread group).
+constexpr int kExecThreads = 256;
+constexpr int kWorkerThreads = 32 + kExecThreads;
+constexpr int kBufs = 2;  // task buffers between the fetcher and the executors
+// Named barriers: 0 = whole CTA, 1 = executor group (task bodies),
+// 2+b = buffer b full (fetcher arrives, executors wait),
+// 4+b = buffer b empty (executors arrive, fetcher waits).
+constexpr int kBarFull = 2, kBarEmpty = 4;
+// Per-CTA cache of resolved table entries, tagged with the version they were
+// resolved under: an entry of version v is immutable while v is current
+// (the host rewrites a bank only after every epoch moved past it), so a tag
+// hit needs no HBM lookup.
+constexpr int kEntryCache = 64;
+struct CachedEntry {
+  uint64_t version;  // kQuiescent = invalid
+  uint64_t aux;
+  uint32_t op_id;
+  uint32_t kind;
+  int32_t code;
+  uint32_t pad;
+};
+static_assert(sizeof(CachedEntry) == 32, "cache entry is 32 bytes");
+
+// Shared header (kHeaderBytes): tasks | ctls | counters | entry cache.
+struct WorkerHeader {
+  gpuos_task task[kBufs];
+  SharedCtl ctl[kBufs];
+  uint64_t done;      // tasks completed by this CTA (all generations)
+  uint64_t claimed;   // tickets claimed by this CTA (all generations)
+  uint64_t pad[2];
+  CachedEntry cache[kEntryCache];
+};
+static_assert(sizeof(WorkerHeader) <= kHeaderBytes, "worker header overflows");
+
+// Barrier ids must be immediates (a register id makes ptxas reserve all 16).
+template <int ID>
+__device__ __forceinline__ void bar_sync(int n) {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void bar_arrive(int n) {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+__device__ __forceinline__ void buf_wait_full(int b) {
+  if (b == 0) bar_sync<kBarFull>(kWorkerThreads);
+  else bar_sync<kBarFull + 1>(kWorkerThreads);
+}
+__device__ __forceinline__ void buf_mark_full(int b) {
+  if (b == 0) bar_arrive<kBarFull>(kWorkerThreads);
+  else bar_arrive<kBarFull + 1>(kWorkerThreads);
+}
+__device__ __forceinline__ void buf_wait_empty(int b) {
+  if (b == 0) bar_sync<kBarEmpty>(kWorkerThreads);
+  else bar_sync<kBarEmpty + 1>(kWorkerThreads);
+}
+__device__ __forceinline__ void buf_mark_empty(int b) {
+  if (b == 0) bar_arrive<kBarEmpty>(kWorkerThreads);
+  else bar_arrive<kBarEmpty + 1>(kWorkerThreads);
+}
+
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
@@ -99,16 +159,16 @@ __device__ __forceinline__ TableEntry load_entry(const TableEntry* e) {
   return r;
 }
 
-// Host-visible per-worker counts are written lazily by warp 0 lane 0 (the
-// single writer, so posted writes stay monotone): every 16 claims and on every
-// idle poll where they changed, and once more at exit.
+// Host-visible per-worker counts, written only by the fetcher lane 0 while
+// the generation runs (single writer, so posted writes stay monotone) and by
+// the executor leader once at exit.
 struct Mirror {
-  uint64_t claimed = 0, flushed_claimed = 0, flushed_done = 0;
+  uint64_t flushed_claimed = 0, flushed_done = 0;
 };
-__device__ __forceinline__ void flush_mirror(DevState* S, uint32_t w, Mirror& m, uint64_t done) {
-  if (m.claimed != m.flushed_claimed) {
-    st_relaxed_sys(&S->host_claimed[w], m.claimed);  // claimed before done: head >= processed
-    m.flushed_claimed = m.claimed;
+__device__ __forceinline__ void flush_mirror(DevState* S, uint32_t w, Mirror& m, uint64_t claimed, uint64_t done) {
+  if (claimed != m.flushed_claimed) {
+    st_relaxed_sys(&S->host_claimed[w], claimed);  // claimed before done: head >= processed
+    m.flushed_claimed = claimed;
   }
   if (done != m.flushed_done) {
     st_relaxed_sys(&S->host_done[w], done);
@@ -116,23 +176,66 @@ __device__ __forceinline__ void flush_mirror(DevState* S, uint32_t w, Mirror& m,
   }
 }
 
-// Warp 0: claim one ticket, wait for its publication, copy it to shared
-// memory, free the slot, and resolve the op through the versioned table.
+// Resolve op -> (kind, aux, code) under version `ver` (optable.hpp:114-124 +
+// the generation canary, executor.hpp:197-212).  Lane 0 only.
+__device__ __forceinline__ void resolve(DevState* S, uint32_t w, WorkerHeader* H, uint32_t op, uint64_t& ver,
+                                        uint64_t& my_epoch, SharedCtl* ctl) {
+  if (op >= S->table_slots) {
+    ctl->code = GPUOS_OUT_OF_RANGE;
+    ctl->kind = GPUOS_KIND_KILLED;
+    ctl->aux = 0;
+    return;
+  }
+  CachedEntry* ce = &H->cache[op % kEntryCache];
+  if (ce->version == ver && ce->op_id == op) {
+    ctl->code = ce->code;
+    ctl->kind = ce->kind;
+    ctl->aux = ce->aux;
+    return;
+  }
+  int code = GPUOS_OK;
+  TableEntry e;
+  e.kind = 0;
+  e.aux = 0;
+  for (int retry = 0;; ++retry) {
+    e = load_entry(&S->bank[ver & 1][op]);
+    const uint64_t gen = ld_relaxed_gpu(&S->bank_gen[ver & 1]);
+    code = e.status == 1 ? GPUOS_OK : (e.status == 2 ? GPUOS_OPERATOR_KILLED : GPUOS_NOT_INSTALLED);
+    // canary: an entry must carry the generation of its version's bank
+    if (code == GPUOS_OK && gen != ver && retry < 4) {
+      atomicAdd((unsigned long long*)&S->canary_hits, 1ull);
+      ver = stable_snapshot(S, w, ld_acquire_gpu(&S->version));
+      my_epoch = ver;
+      continue;
+    }
+    break;
+  }
+  const uint32_t kind = e.kind < kNumKinds ? e.kind : (uint32_t)GPUOS_KIND_KILLED;
+  ctl->code = code;
+  ctl->kind = kind;
+  ctl->aux = e.aux;
+  ce->version = ver;
+  ce->op_id = op;
+  ce->code = code;
+  ce->kind = kind;
+  ce->aux = e.aux;
+}
+
+// Fetcher warp: claim a ticket, wait for its publication, stage the slot in
+// buffer `b`, free the slot, resolve the op.  Returns false at the sentinel
+// (or past the stop position), with ctl->exit set.
 //
 // PCIe discipline (measured, profiles/r01_phases_*.log): every host-memory
-// access costs a round trip through the VM's PCIe path and a fence that
-// follows a sysmem store waits for it, so this path issues one slot read, one
-// slot-free store, the tail read only when the ticket is past the hint, and no
-// fence.  Task inputs need no acquire fence because the worker module is
-// compiled with -dlcm=cg: global loads bypass the (non-coherent) L1.
-//
-// Epochs: an idle worker does not park; every 16 polls it re-reads the table
-// version and republishes its epoch when the version moved, so an install's
-// epoch wait (optable.hpp:591-600) completes within a few polls while the
-// common claim path pays no system-scope fence when the version is unchanged.
-__device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_task* task, SharedCtl* ctl,
-                                                uint64_t& my_epoch, Mirror& mir, const volatile uint64_t* done,
-                                                int lane) {
+// access costs a round trip through the PCIe path and a fence that follows a
+// sysmem store waits for it, so this path issues one slot read (the version
+// word rides along on lane 31), one slot-free store, the tail read only when
+// the ticket is past the hint, and no fence.  Task inputs need no acquire
+// fence because the worker module is compiled with -dlcm=cg: global loads
+// bypass the (non-coherent) L1.
+__device__ __forceinline__ bool fetch(DevState* S, uint32_t w, WorkerHeader* H, int b, uint64_t& my_epoch,
+                                      Mirror& mir, int lane) {
+  gpuos_task* task = &H->task[b];
+  SharedCtl* ctl = &H->ctl[b];
   uint64_t pos = 0;
   if (lane == 0) {
     while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
@@ -143,6 +246,7 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
   const char* slot = (const char*)(S->ring + (pos & S->mask));
   uint32_t spins = 0, expn = 0;
   uint4 v = make_uint4(0, 0, 0, 0);
+  uint64_t ver = 0;
   for (;;) {
     const uint64_t sp = ld_relaxed_gpu(&S->stop_pos);
     if (pos > sp) {
@@ -151,7 +255,8 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
         my_epoch = kQuiescent;
         ctl->exit = 1;
       }
-      return;
+      __syncwarp();
+      return false;
     }
     // Only tickets within two of the highest tail seen on the device read
     // PCIe; the rest watch the HBM hint.  Progress: the ticket equal to the
@@ -163,6 +268,7 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
       if (lane < 24) v = ld_volatile_v4(slot + 16 * lane);
       uint64_t tail = 0;
       if (lane == 24 && pos >= h) tail = ld_relaxed_sys(S->host_tail);
+      if (lane == 31) ver = ld_acquire_gpu(&S->version);
       const uint64_t pub = ((uint64_t)__shfl_sync(0xffffffffu, v.y, 0) << 32) | __shfl_sync(0xffffffffu, v.x, 0);
       tail = shfl64(tail, 24);
       if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
@@ -170,8 +276,8 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
         const uint64_t w0 = ((uint64_t)v.y << 32) | v.x, w1 = ((uint64_t)v.w << 32) | v.z;
         uint64_t part = 0;
         if (lane < 24) {
-          part = slot_mix(w0, 2 * lane);
-          if (lane != 3) part += slot_mix(w1, 2 * lane + 1);  // word 7 is the checksum
+          part = slot_term(w0, 2 * lane);
+          if (lane != 3) part += slot_term(w1, 2 * lane + 1);  // word 7 is the checksum
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -183,10 +289,10 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
     }
     ++spins;
     if (lane == 0) {
-      flush_mirror(S, w, mir, *done);  // idle: make counts visible to wait_all / peek
+      flush_mirror(S, w, mir, H->claimed, *(volatile uint64_t*)&H->done);  // idle: counts for wait_all / peek
       if ((spins & 15) == 0) {
-        const uint64_t ver = ld_acquire_gpu(&S->version);
-        if (ver != my_epoch) my_epoch = stable_snapshot(S, w, ver);
+        const uint64_t cur = ld_acquire_gpu(&S->version);
+        if (cur != my_epoch) my_epoch = stable_snapshot(S, w, cur);
         if (spins == S->spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
       }
     }
@@ -196,14 +302,15 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
     }
   }
   const uint64_t t_seen = globaltimer();
-  // fetched: stage the descriptor in shared memory
+  ver = shfl64(ver, 31);
+  // stage the descriptor in shared memory
   if (lane < 24) reinterpret_cast<uint4*>(task)[lane] = v;
   __syncwarp();
   if (lane == 0) {
     // free the slot for the producer's next lap (queue.hpp:248)
     st_relaxed_sys((uint64_t*)(S->ring + (pos & S->mask)), pos + S->cap);
-    ++mir.claimed;
-    if ((mir.claimed & 15) == 0) flush_mirror(S, w, mir, *done);
+    const uint64_t claimed = ++H->claimed;
+    if ((claimed & 15) == 0) flush_mirror(S, w, mir, claimed, *(volatile uint64_t*)&H->done);
     ctl->t_fenced = globaltimer();
     ctl->pos = pos;
     ctl->exit = 0;
@@ -215,56 +322,31 @@ __device__ __forceinline__ void claim_and_fetch(DevState* S, uint32_t w, gpuos_t
       my_epoch = kQuiescent;
       ctl->exit = 1;
     } else {
-      uint64_t ver = ld_acquire_gpu(&S->version);
       if (ver != my_epoch) ver = stable_snapshot(S, w, ver);
       my_epoch = ver;
-      const uint32_t op = task->op_id;
-      int code = GPUOS_OK;
-      TableEntry e;
-      e.kind = 0;
-      e.aux = 0;
-      for (int retry = 0;; ++retry) {
-        if (op >= S->table_slots) {
-          code = GPUOS_OUT_OF_RANGE;
-          break;
-        }
-        e = load_entry(&S->bank[ver & 1][op]);
-        const uint64_t gen = ld_relaxed_gpu(&S->bank_gen[ver & 1]);
-        code = e.status == 1 ? GPUOS_OK : (e.status == 2 ? GPUOS_OPERATOR_KILLED : GPUOS_NOT_INSTALLED);
-        // canary: an entry must carry the generation of its version's bank
-        if (code == GPUOS_OK && gen != ver && retry < 4) {
-          atomicAdd((unsigned long long*)&S->canary_hits, 1ull);
-          ver = stable_snapshot(S, w, ld_acquire_gpu(&S->version));
-          my_epoch = ver;
-          continue;
-        }
-        break;
-      }
+      resolve(S, w, H, task->op_id, ver, my_epoch, ctl);
       ctl->version = ver;
-      ctl->code = code;
-      ctl->kind = e.kind < kNumKinds ? e.kind : (uint32_t)GPUOS_KIND_KILLED;
-      ctl->aux = e.aux;
       ctl->t_deq = globaltimer();
     }
   }
   __syncwarp();
+  return ctl->exit == 0;
 }
 
-// Completion (runtime.hpp:628-639) by lane 0 of one of warps 1..7, rotating
-// per task, while warp 0 already claims the next task into the other buffer.
-// Every thread's outputs are ordered before it by the barrier; the gpu-scope
-// release puts them in L2 (where the host's copy engine reads) before the
-// word is posted.  Rotating the completer means the fence never waits on a
-// sysmem store issued by the same warp just before.
-__device__ __forceinline__ void complete_task(DevState* S, uint32_t w, const gpuos_task* task, const SharedCtl* ctl,
-                                              int code, volatile uint64_t* done, uint64_t& executed) {
+// Completion (runtime.hpp:628-639) by lane 0 of one executor warp, rotating
+// per task so that its gpu-scope fence never waits on a sysmem store the same
+// warp issued just before.  The group barrier orders every executor's output
+// writes before the fence; the release puts them in L2 (where the host's copy
+// engine reads) before the word is posted.
+__device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHeader* H, const gpuos_task* task,
+                                              const SharedCtl* ctl, int code, uint64_t& executed) {
   const uint64_t t_end = globaltimer();
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
   if (task->done_cell) {
     const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
     st_relaxed_sys((uint64_t*)task->done_cell, word);
   }
-  *done = *done + 1;
+  *(volatile uint64_t*)&H->done = H->done + 1;
   atomicAdd((unsigned long long*)&S->processed, 1ull);
   if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);
   atomicAdd((unsigned long long*)&S->per_op[task->op_id < 256 ? task->op_id : 255], 1ull);
@@ -291,22 +373,44 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, const gpu
   if (ye > 0 && executed % ye == 0) __nanosleep(1000);  // yield_every (executor.hpp:190-193)
 }
 
-extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevState* S) {
+// One persistent generation.  Warp 0 runs ahead of the executors by up to
+// kBufs tasks, so the PCIe round trip of the next claim overlaps the body and
+// completion of the current one.
+extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_kernel(DevState* S) {
   extern __shared__ __align__(128) char smem[];
-  // two task buffers: warp 0 fetches task k+1 while task k is being completed
-  gpuos_task* tasks[2] = {reinterpret_cast<gpuos_task*>(smem), reinterpret_cast<gpuos_task*>(smem + kTaskBytes)};
-  // header layout: task[0] | task[1] | ctl[0] | ctl[1] | done counter
-  static_assert(2 * kTaskBytes + 2 * kCtlStride + 8 <= kHeaderBytes, "worker header overflows");
-  SharedCtl* ctls[2] = {reinterpret_cast<SharedCtl*>(smem + 2 * kTaskBytes),
-                        reinterpret_cast<SharedCtl*>(smem + 2 * kTaskBytes + kCtlStride)};
-  volatile uint64_t* done = reinterpret_cast<volatile uint64_t*>(smem + 2 * kTaskBytes + 2 * kCtlStride);
+  WorkerHeader* H = reinterpret_cast<WorkerHeader*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t w = blockIdx.x;
+  if (tid == 0) {
+    // continue the host-visible counts across kernel generations
+    H->claimed = ld_relaxed_sys(&S->host_claimed[w]);
+    H->done = ld_relaxed_sys(&S->host_done[w]);
+  }
+  for (int i = tid; i < kEntryCache; i += blockDim.x) {
+    H->cache[i].version = kQuiescent;
+    H->cache[i].op_id = 0xffffffffu;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // ---------------- fetcher ----------------
+    uint64_t my_epoch = kQuiescent;
+    Mirror mir;
+    mir.flushed_claimed = H->claimed;
+    mir.flushed_done = H->done;
+    for (uint32_t k = 0;; ++k) {
+      const int b = (int)(k % kBufs);
+      if (k >= kBufs) buf_wait_empty(b);
+      const bool more = fetch(S, w, H, b, my_epoch, mir, lane);
+      buf_mark_full(b);
+      if (!more) return;
+    }
+  }
+  // ---------------- executors ----------------
   uint32_t dyn;
   asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
   Ctx ctx;
-  ctx.tid = tid;
-  ctx.nthreads = blockDim.x;
+  ctx.tid = tid - 32;
+  ctx.nthreads = kExecThreads;
   ctx.part = 0;
   ctx.nparts = 1;
   ctx.bar_id = 1;
@@ -314,24 +418,20 @@ extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevStat
   ctx.smem_bytes = (int)dyn - (int)kHeaderBytes;
   ctx.aux = 0;
   ctx.flags = 0;
-  uint64_t my_epoch = kQuiescent, executed = 0;
-  Mirror mir;
-  if (tid == 0) {
-    // continue the host-visible counts across kernel generations
-    mir.claimed = mir.flushed_claimed = ld_relaxed_sys(&S->host_claimed[w]);
-    mir.flushed_done = ld_relaxed_sys(&S->host_done[w]);
-    *done = mir.flushed_done;
-  }
-  __syncthreads();
-  const int nwarps = blockDim.x >> 5;
-  uint32_t k = 0;
-  for (;; ++k) {
-    gpuos_task* task = tasks[k & 1];
-    SharedCtl* ctl = ctls[k & 1];
-    if (warp == 0) claim_and_fetch(S, w, task, ctl, my_epoch, mir, done, lane);
-    __syncthreads();
+  uint64_t executed = 0;
+  const int nexec_warps = kExecThreads / 32;
+  for (uint32_t k = 0;; ++k) {
+    const int b = (int)(k % kBufs);
+    buf_wait_full(b);
+    const gpuos_task* task = &H->task[b];
+    const SharedCtl* ctl = &H->ctl[b];
     if (ctl->exit) {
-      if (tid == 0) flush_mirror(S, w, mir, *done);  // final counts for wait_all and the next generation
+      if (ctx.tid == 0) {
+        // final counts for wait_all and the next generation (the fetcher has
+        // returned, so this thread is the only writer now)
+        st_relaxed_sys(&S->host_claimed[w], H->claimed);
+        st_relaxed_sys(&S->host_done[w], H->done);
+      }
       return;
     }
     int code = ctl->code;
@@ -341,8 +441,10 @@ extern "C" __global__ void __launch_bounds__(256, 2) gpuos_worker_kernel(DevStat
       const OpFn fn = g_kind_fns[ctl->kind];
       code = fn(task, &ctx);
     }
-    __syncthreads();
-    if (lane == 0 && warp == 1 + (int)(k % (uint32_t)(nwarps - 1))) complete_task(S, w, task, ctl, code, done, executed);
+    bar_sync<1>(kExecThreads);
+    if (lane == 0 && warp == 1 + (int)(k % (uint32_t)nexec_warps)) complete_task(S, w, H, task, ctl, code, executed);
+    __syncwarp();
+    buf_mark_empty(b);
   }
 }
 
@@ -435,6 +537,7 @@ static TaskKernel task_kernel_for(uint32_t kind) {
 }
 
 uint32_t worker_smem_bytes() { return kHeaderBytes + kScratchBytes; }
+uint32_t worker_threads() { return kWorkerThreads; }
 
 // Lazy module loading blocks while the persistent kernel is resident
 // (measured: profiles/r01_probe2_lazy.log), so every kernel is loaded and
@@ -453,6 +556,10 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
     cudaFuncGetAttributes(&fa, f);
   }
   cudaFuncGetAttributes(&fa, gpuos_clock_probe);
+}
+
+cudaError_t worker_occupancy(int* per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, gpuos_worker_kernel, kWorkerThreads, worker_smem_bytes());
 }
 
 cudaError_t launch_worker(DevState* s, uint32_t workers, uint32_t threads, uint32_t smem, cudaStream_t st) {
