@@ -25,7 +25,7 @@ cpp-tests: build/cpp/test_runtime build/cpp/test_host
 
 $(OBJ)/worker.o: $(CSRC)/worker.cu $(DEV_HDRS)
 	@mkdir -p $(OBJ)
-	$(NVCC) $(NVFLAGS) -Xptxas -dlcm=cg -c $< -o $@
+	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(OBJ)/capi.o: $(CSRC)/capi.cu $(DEV_HDRS)
 	@mkdir -p $(OBJ)

@@ -294,8 +294,9 @@ int gpuos_trace_enable(gpuos_dev* dev, int on);
 int gpuos_trace_snapshot(gpuos_dev* dev, gpuos_tracepoint* out, uint64_t cap, uint64_t* n);
 
 /* Per-task phase stamps of the same records, all on the host steady clock:
- * commit, ticket taken by the claiming worker, publication observed, table
- * resolved (dequeue), body finished, completion posted. */
+ * commit, fetcher starts polling the ticket, publication observed, task
+ * staged and resolved (dequeue), body finished, completion posted;
+ * `reserved` = ns from dequeue until the executor group picked it up. */
 typedef struct gpuos_trace_phase {
   uint64_t seq;
   uint64_t enqueue_ns;

@@ -1004,7 +1004,7 @@ int gpuos_trace_phases(gpuos_dev* d, gpuos_trace_phase* out, uint64_t cap, uint6
     p.end_ns = h(r.dequeue_gt + r.exec_ns);
     p.done_ns = h(r.t_done);
     p.worker = (uint32_t)r.worker;
-    p.reserved = (uint32_t)(r.pad > r.t_seen ? r.pad - r.t_seen : 0);  // seen -> fenced ns
+    p.reserved = (uint32_t)(r.pad > r.dequeue_gt ? r.pad - r.dequeue_gt : 0);  // staged -> executor wake ns
   }
   *n = k;
   return GPUOS_OK;

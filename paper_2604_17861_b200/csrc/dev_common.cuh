@@ -210,6 +210,41 @@ __device__ __forceinline__ bool same_shape(const gpuos_view& a, const gpuos_view
   return true;
 }
 __device__ __forceinline__ bool is_float_dt(int dt) { return dt != GPUOS_I32; }
+// Row-major contiguous (unit dims ignored): element e lives at offset e.
+__device__ __forceinline__ bool dense_view(const gpuos_view& v) {
+  int64_t expect = 1;
+  for (int d = v.rank - 1; d >= 0; --d) {
+    if (v.extents[d] == 1) continue;
+    if (v.strides[d] != expect) return false;
+    expect *= v.extents[d];
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Task plan: a shape classification computed once per task before the body
+// runs (by the fetcher warp in the worker, by the kernel prologue on the
+// conventional path) and handed over in Ctx::flags.  kPlanDenseSame means
+// every operand view (output + n_inputs inputs) bound cleanly, has the
+// output's dtype and shape, and is row-major dense: every reference check an
+// elementwise body performs would pass, so it may go straight to its dense
+// loop.  The plan is only a hint; bodies must still be correct without it.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPlanDenseSame = 1u << 31;
+
+// View `k`'s part of the classification (one lane per view).
+__device__ __forceinline__ bool plan_view_ok(const gpuos_task* t, int k) {
+  const gpuos_view& o = t->views[0];
+  const gpuos_view& v = t->views[k];
+  return v.status == GPUOS_VIEW_OK && v.dtype == o.dtype && same_shape(v, o) && dense_view(v);
+}
+// Warp-wide classification: lanes 0..n_inputs each check one view.
+__device__ __forceinline__ uint32_t plan_task_warp(const gpuos_task* t, int lane) {
+  const int nv = 1 + (int)t->n_inputs;
+  const bool ok = lane >= nv || nv > 1 + GPUOS_MAX_INPUTS || plan_view_ok(t, lane);
+  const unsigned all = __all_sync(0xffffffffu, ok);
+  return (all && nv <= 1 + GPUOS_MAX_INPUTS) ? kPlanDenseSame : 0u;
+}
 
 // ---------------------------------------------------------------------------
 // Fast unsigned divmod by an invariant divisor (n < 2^31).

@@ -134,10 +134,34 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
 
 // Checks in the reference order (ops.hpp:133-153), then dispatch on dtype.
 template <class F>
+__device__ __forceinline__ bool ew_dense_dispatch(const gpuos_task* t, const Ctx* c, int dt, int64_t n, F f) {
+  switch (dt) {
+    case GPUOS_F32: ew_dense<GPUOS_F32>(t, c, n, f); return true;
+    case GPUOS_F64: ew_dense<GPUOS_F64>(t, c, n, f); return true;
+    case GPUOS_I32: ew_dense<GPUOS_I32>(t, c, n, f); return true;
+    case GPUOS_F16: ew_dense<GPUOS_F16>(t, c, n, f); return true;
+    case GPUOS_BF16: ew_dense<GPUOS_BF16>(t, c, n, f); return true;
+    default: return false;
+  }
+}
+
+template <class F>
 __device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
   constexpr int A = F::A;
   if (t->n_inputs != A) return GPUOS_ARITY_ERROR;
   const gpuos_view& out = t->views[0];
+  if (c->flags & kPlanDenseSame) {
+    // planned: same dtype/shape, dense, bound; only the dtype class and the
+    // size ceiling remain to check (ops.hpp:133-153 order preserved)
+    const int dt = out.dtype;
+    if (!allow_int && dt == GPUOS_I32) return GPUOS_DTYPE_MISMATCH;
+    const int64_t n = numel(out);
+    if (n == 0) return GPUOS_OK;
+    if (n < ((int64_t)1 << 31)) {
+      F f;
+      return ew_dense_dispatch(t, c, dt, n, f) ? GPUOS_OK : GPUOS_DTYPE_MISMATCH;
+    }
+  }
   if (!allow_int && out.dtype == GPUOS_I32) return GPUOS_DTYPE_MISMATCH;
   for (int k = 0; k < A; ++k)
     if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
@@ -152,9 +176,14 @@ __device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
   }
   const int b = bind_code(out);
   if (b) return b;
+  F f;
+  // common case first: every operand dense with the output's shape, so the
+  // strided iteration space (and its divmod setup) is not needed
+  bool simple = dense_view(out);
+  for (int k = 0; k < A && simple; ++k) simple = same_shape(t->views[1 + k], out) && dense_view(t->views[1 + k]);
+  if (simple) return ew_dense_dispatch(t, c, out.dtype, n, f) ? GPUOS_OK : GPUOS_DTYPE_MISMATCH;
   Space s;
   build_space(s, out, A, st);
-  F f;
   switch (out.dtype) {
 #define GPUOS_EW_CASE(DT)                        \
   case DT:                                       \
@@ -174,10 +203,34 @@ __device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
   return GPUOS_OK;
 }
 
-__device__ __noinline__ int op_add(const gpuos_task* t, const Ctx* c) { return ew_body<FAdd>(t, c, true); }
-__device__ __noinline__ int op_mul(const gpuos_task* t, const Ctx* c) { return ew_body<FMul>(t, c, true); }
-__device__ __noinline__ int op_relu(const gpuos_task* t, const Ctx* c) { return ew_body<FRelu>(t, c, true); }
-__device__ __noinline__ int op_gelu(const gpuos_task* t, const Ctx* c) { return ew_body<FGelu>(t, c, false); }
+// General path: every reference check, every dtype, strided/broadcast.
+template <class F>
+__device__ __noinline__ int ew_general(const gpuos_task* t, const Ctx* c, bool allow_int) {
+  return ew_body<F>(t, c, allow_int);
+}
+
+// Entry points in the jump table.  A planned dense f32 task (the common small
+// op) runs its loop right here; everything else goes through ew_general.
+// Keeping the heavy general path out of line keeps these functions' register
+// footprint -- and so the callee-saved spills of every indirect call -- small
+// (measured: tools/probe/body_bench.cu).
+template <class F>
+__device__ __forceinline__ int ew_entry(const gpuos_task* t, const Ctx* c, bool allow_int) {
+  if ((c->flags & kPlanDenseSame) && t->n_inputs == F::A && t->views[0].dtype == GPUOS_F32) {
+    const int64_t n = numel(t->views[0]);
+    if (n > 0 && n < ((int64_t)1 << 31)) {
+      F f;
+      ew_dense<GPUOS_F32>(t, c, n, f);
+      return GPUOS_OK;
+    }
+  }
+  return ew_general<F>(t, c, allow_int);
+}
+
+__device__ __noinline__ int op_add(const gpuos_task* t, const Ctx* c) { return ew_entry<FAdd>(t, c, true); }
+__device__ __noinline__ int op_mul(const gpuos_task* t, const Ctx* c) { return ew_entry<FMul>(t, c, true); }
+__device__ __noinline__ int op_relu(const gpuos_task* t, const Ctx* c) { return ew_entry<FRelu>(t, c, true); }
+__device__ __noinline__ int op_gelu(const gpuos_task* t, const Ctx* c) { return ew_general<FGelu>(t, c, false); }
 
 // ---------------------------------------------------------------------------
 // Injected operators: a verified stack-machine program evaluated in double per
@@ -254,17 +307,23 @@ __device__ __noinline__ int op_program(const gpuos_task* t, const Ctx* c) {
   const int64_t n = numel(out);
   if (n == 0) return GPUOS_OK;
   if (n >= (int64_t)1 << 31) return GPUOS_TOO_LARGE;
-  int64_t st[GPUOS_MAX_INPUTS][GPUOS_MAX_RANK];
-  for (int k = 0; k < arity; ++k) {
-    if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
-    if (!broadcast_strides(t->views[1 + k], out, st[k])) return GPUOS_INCOMPATIBLE_SHAPES;
-    const int b = bind_code(t->views[1 + k]);
-    if (b) return b;
-  }
-  const int b = bind_code(out);
-  if (b) return b;
   Space s;
-  build_space(s, out, arity, st);
+  if (c->flags & kPlanDenseSame) {
+    s.dense = true;  // planned: dtypes, shapes, binds already known good
+    s.nops = arity + 1;
+    s.rank = 0;
+  } else {
+    int64_t st[GPUOS_MAX_INPUTS][GPUOS_MAX_RANK];
+    for (int k = 0; k < arity; ++k) {
+      if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+      if (!broadcast_strides(t->views[1 + k], out, st[k])) return GPUOS_INCOMPATIBLE_SHAPES;
+      const int b = bind_code(t->views[1 + k]);
+      if (b) return b;
+    }
+    const int b = bind_code(out);
+    if (b) return b;
+    build_space(s, out, arity, st);
+  }
   // stage the program in shared memory (<= GPUOS_MAX_PROGRAM instructions)
   const int n_instr = (int)h->n_instr;
   gpuos_instr* code = (gpuos_instr*)c->smem;

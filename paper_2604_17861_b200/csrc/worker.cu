@@ -57,29 +57,42 @@ struct SharedCtl {
   uint64_t t_deq;
   uint64_t t_ticket;
   uint64_t t_seen;
-  uint64_t t_fenced;
+  uint64_t t_fenced;     // executor group woke for this task
+  uint64_t t_end;        // body finished (executor group)
+  uint64_t yield_every;  // live knobs sampled by the fetcher with the slot read
+  uint32_t trace_on;
   uint32_t kind;
   int32_t code;
   uint32_t exit;
+  uint32_t plan;  // kPlanDenseSame etc. (dev_common.cuh)
   uint32_t pad;
 };
 
 constexpr uint32_t kCtlStride = 112;
 static_assert(sizeof(SharedCtl) <= kCtlStride, "SharedCtl must fit its stride");
 
-// Worker CTA shape: warp 0 fetches, warps 1..8 execute (one 256-thread group).
+// Worker CTA shape (warp-specialised pipeline, one task per buffer):
+//   warp 0      fetcher   : claim ticket -> PCIe slot read -> stage -> resolve
+//   warps 1..8  executors : the task body as one 256-thread group
+//   warp 9      completer : output fence -> completion word -> counters
+// so the PCIe round trip of the next claim and the completion fence of the
+// previous task both overlap the current body.
 constexpr int kExecThreads = 256;
-constexpr int kWorkerThreads = 32 + kExecThreads;
-constexpr int kBufs = 2;  // task buffers between the fetcher and the executors
+constexpr int kWorkerThreads = 32 + kExecThreads + 32;
+constexpr int kCompleterWarp = 1 + kExecThreads / 32;
+constexpr int kBufs = 3;
 // Named barriers: 0 = whole CTA, 1 = executor group (task bodies),
-// 2+b = buffer b full (fetcher arrives, executors wait),
-// 4+b = buffer b empty (executors arrive, fetcher waits).
-constexpr int kBarFull = 2, kBarEmpty = 4;
+// FULL[b]  = 2+b : fetcher arrives, executors wait      (32 + 256)
+// DONE[b]  = 5+b : executors arrive, completer waits    (256 + 32)
+// EMPTY[b] = 8+b : completer arrives, fetcher waits     (32 + 32)
+constexpr int kBarFull = 2, kBarDone = 5, kBarEmpty = 8;
+constexpr int kFullCount = 32 + kExecThreads, kDoneCount = kExecThreads + 32, kEmptyCount = 64;
 // Per-CTA cache of resolved table entries, tagged with the version they were
 // resolved under: an entry of version v is immutable while v is current
 // (the host rewrites a bank only after every epoch moved past it), so a tag
 // hit needs no HBM lookup.
 constexpr int kEntryCache = 64;
+constexpr uint64_t kNoTicket = ~0ull;
 struct CachedEntry {
   uint64_t version;  // kQuiescent = invalid
   uint64_t aux;
@@ -94,8 +107,8 @@ static_assert(sizeof(CachedEntry) == 32, "cache entry is 32 bytes");
 struct WorkerHeader {
   gpuos_task task[kBufs];
   SharedCtl ctl[kBufs];
-  uint64_t done;      // tasks completed by this CTA (all generations)
-  uint64_t claimed;   // tickets claimed by this CTA (all generations)
+  uint64_t done;     // tasks completed by this CTA (all generations)
+  uint64_t claimed;  // tickets claimed by this CTA (all generations)
   uint64_t pad[2];
   CachedEntry cache[kEntryCache];
 };
@@ -110,33 +123,42 @@ template <int ID>
 __device__ __forceinline__ void bar_arrive(int n) {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
 }
-__device__ __forceinline__ void buf_wait_full(int b) {
-  if (b == 0) bar_sync<kBarFull>(kWorkerThreads);
-  else bar_sync<kBarFull + 1>(kWorkerThreads);
+template <int BASE, int N>
+__device__ __forceinline__ void buf_sync(int b) {
+  if (b == 0) bar_sync<BASE>(N);
+  else if (b == 1) bar_sync<BASE + 1>(N);
+  else bar_sync<BASE + 2>(N);
 }
-__device__ __forceinline__ void buf_mark_full(int b) {
-  if (b == 0) bar_arrive<kBarFull>(kWorkerThreads);
-  else bar_arrive<kBarFull + 1>(kWorkerThreads);
-}
-__device__ __forceinline__ void buf_wait_empty(int b) {
-  if (b == 0) bar_sync<kBarEmpty>(kWorkerThreads);
-  else bar_sync<kBarEmpty + 1>(kWorkerThreads);
-}
-__device__ __forceinline__ void buf_mark_empty(int b) {
-  if (b == 0) bar_arrive<kBarEmpty>(kWorkerThreads);
-  else bar_arrive<kBarEmpty + 1>(kWorkerThreads);
+template <int BASE, int N>
+__device__ __forceinline__ void buf_arrive(int b) {
+  if (b == 0) bar_arrive<BASE>(N);
+  else if (b == 1) bar_arrive<BASE + 1>(N);
+  else bar_arrive<BASE + 2>(N);
 }
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
+// Constant per generation: read once from DevState at kernel start.
+struct WConst {
+  const char* ring;
+  uint64_t mask, cap;
+  const uint64_t* host_tail;
+  uint64_t* host_done;
+  uint64_t* host_claimed;
+  uint64_t* host_epoch;
+  uint64_t* dev_epoch;
+  TableEntry* bank[2];
+  uint32_t table_slots, spin_iterations, backoff_max_exp;
+};
+
 // Publish-then-revalidate (executor.hpp:133-141): the epoch slot holds the
 // version dispatched under before any bank is read.
-__device__ __forceinline__ uint64_t stable_snapshot(DevState* S, uint32_t w, uint64_t v) {
+__device__ __forceinline__ uint64_t stable_snapshot(DevState* S, const WConst& K, uint32_t w, uint64_t v) {
   for (;;) {
-    st_relaxed_gpu(&S->dev_epoch[w], v);
-    st_relaxed_sys(&S->host_epoch[w], v);
+    st_relaxed_gpu(&K.dev_epoch[w], v);
+    st_relaxed_sys(&K.host_epoch[w], v);
     fence_sc_sys();
     const uint64_t now = ld_acquire_gpu(&S->version);
     if (now == v) return v;
@@ -144,9 +166,9 @@ __device__ __forceinline__ uint64_t stable_snapshot(DevState* S, uint32_t w, uin
   }
 }
 
-__device__ __forceinline__ void quiesce(DevState* S, uint32_t w) {
-  st_relaxed_gpu(&S->dev_epoch[w], kQuiescent);
-  st_relaxed_sys(&S->host_epoch[w], kQuiescent);
+__device__ __forceinline__ void quiesce(const WConst& K, uint32_t w) {
+  st_relaxed_gpu(&K.dev_epoch[w], kQuiescent);
+  st_relaxed_sys(&K.host_epoch[w], kQuiescent);
 }
 
 __device__ __forceinline__ TableEntry load_entry(const TableEntry* e) {
@@ -159,28 +181,28 @@ __device__ __forceinline__ TableEntry load_entry(const TableEntry* e) {
   return r;
 }
 
-// Host-visible per-worker counts, written only by the fetcher lane 0 while
-// the generation runs (single writer, so posted writes stay monotone) and by
-// the executor leader once at exit.
+// Host-visible per-worker counts, written only by fetcher lane 0 (single
+// writer, so the posted writes stay monotone on the host).
 struct Mirror {
   uint64_t flushed_claimed = 0, flushed_done = 0;
 };
-__device__ __forceinline__ void flush_mirror(DevState* S, uint32_t w, Mirror& m, uint64_t claimed, uint64_t done) {
+__device__ __forceinline__ void flush_mirror(const WConst& K, uint32_t w, Mirror& m, uint64_t claimed,
+                                             uint64_t done) {
   if (claimed != m.flushed_claimed) {
-    st_relaxed_sys(&S->host_claimed[w], claimed);  // claimed before done: head >= processed
+    st_relaxed_sys(&K.host_claimed[w], claimed);  // claimed before done: head >= processed
     m.flushed_claimed = claimed;
   }
   if (done != m.flushed_done) {
-    st_relaxed_sys(&S->host_done[w], done);
+    st_relaxed_sys(&K.host_done[w], done);
     m.flushed_done = done;
   }
 }
 
 // Resolve op -> (kind, aux, code) under version `ver` (optable.hpp:114-124 +
 // the generation canary, executor.hpp:197-212).  Lane 0 only.
-__device__ __forceinline__ void resolve(DevState* S, uint32_t w, WorkerHeader* H, uint32_t op, uint64_t& ver,
-                                        uint64_t& my_epoch, SharedCtl* ctl) {
-  if (op >= S->table_slots) {
+__device__ __forceinline__ void resolve(DevState* S, const WConst& K, uint32_t w, WorkerHeader* H, uint32_t op,
+                                        uint64_t& ver, uint64_t& my_epoch, SharedCtl* ctl) {
+  if (op >= K.table_slots) {
     ctl->code = GPUOS_OUT_OF_RANGE;
     ctl->kind = GPUOS_KIND_KILLED;
     ctl->aux = 0;
@@ -198,13 +220,13 @@ __device__ __forceinline__ void resolve(DevState* S, uint32_t w, WorkerHeader* H
   e.kind = 0;
   e.aux = 0;
   for (int retry = 0;; ++retry) {
-    e = load_entry(&S->bank[ver & 1][op]);
+    e = load_entry(&K.bank[ver & 1][op]);
     const uint64_t gen = ld_relaxed_gpu(&S->bank_gen[ver & 1]);
     code = e.status == 1 ? GPUOS_OK : (e.status == 2 ? GPUOS_OPERATOR_KILLED : GPUOS_NOT_INSTALLED);
     // canary: an entry must carry the generation of its version's bank
     if (code == GPUOS_OK && gen != ver && retry < 4) {
       atomicAdd((unsigned long long*)&S->canary_hits, 1ull);
-      ver = stable_snapshot(S, w, ld_acquire_gpu(&S->version));
+      ver = stable_snapshot(S, K, w, ld_acquire_gpu(&S->version));
       my_epoch = ver;
       continue;
     }
@@ -221,37 +243,31 @@ __device__ __forceinline__ void resolve(DevState* S, uint32_t w, WorkerHeader* H
   ce->aux = e.aux;
 }
 
-// Fetcher warp: claim a ticket, wait for its publication, stage the slot in
-// buffer `b`, free the slot, resolve the op.  Returns false at the sentinel
-// (or past the stop position), with ctl->exit set.
+// Fetcher: wait for ticket `pos`'s publication, stage the slot in buffer
+// `b`, free the slot, resolve the op.  `next` is the ticket claimed ahead for
+// the following call.  Returns false at the sentinel (or past the stop
+// position), with ctl->exit set.
 //
 // PCIe discipline (measured, profiles/r01_phases_*.log): every host-memory
 // access costs a round trip through the PCIe path and a fence that follows a
 // sysmem store waits for it, so this path issues one slot read (the version
-// word rides along on lane 31), one slot-free store, the tail read only when
-// the ticket is past the hint, and no fence.  Task inputs need no acquire
-// fence because the worker module is compiled with -dlcm=cg: global loads
-// bypass the (non-coherent) L1.
-__device__ __forceinline__ bool fetch(DevState* S, uint32_t w, WorkerHeader* H, int b, uint64_t& my_epoch,
+// and the live knobs ride along on lanes 25..31), one slot-free store, the
+// tail read only when the ticket is past the hint, and one gpu-scope acquire
+// fence once the slot validated (it invalidates this SM's L1 for the task).
+__device__ __forceinline__ bool fetch(DevState* S, const WConst& K, uint32_t w, WorkerHeader* H, int b,
+                                      uint64_t pos, uint64_t t_ticket, uint64_t& next, uint64_t& my_epoch,
                                       Mirror& mir, int lane) {
   gpuos_task* task = &H->task[b];
   SharedCtl* ctl = &H->ctl[b];
-  uint64_t pos = 0;
-  if (lane == 0) {
-    while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
-    pos = atomicAdd((unsigned long long*)&S->claim, 1ull);
-  }
-  pos = shfl64(pos, 0);
-  const uint64_t t_ticket = globaltimer();
-  const char* slot = (const char*)(S->ring + (pos & S->mask));
+  const char* slot = K.ring + (pos & K.mask) * kTaskBytes;
   uint32_t spins = 0, expn = 0;
   uint4 v = make_uint4(0, 0, 0, 0);
-  uint64_t ver = 0;
+  uint64_t aux = 0;  // lane 31: version, lane 30: yield_every, lane 29: trace_on
   for (;;) {
     const uint64_t sp = ld_relaxed_gpu(&S->stop_pos);
     if (pos > sp) {
       if (lane == 0) {
-        quiesce(S, w);
+        quiesce(K, w);
         my_epoch = kQuiescent;
         ctl->exit = 1;
       }
@@ -267,8 +283,10 @@ __device__ __forceinline__ bool fetch(DevState* S, uint32_t w, WorkerHeader* H, 
     if (near) {
       if (lane < 24) v = ld_volatile_v4(slot + 16 * lane);
       uint64_t tail = 0;
-      if (lane == 24 && pos >= h) tail = ld_relaxed_sys(S->host_tail);
-      if (lane == 31) ver = ld_acquire_gpu(&S->version);
+      if (lane == 24 && pos >= h) tail = ld_relaxed_sys(K.host_tail);
+      if (lane == 31) aux = ld_acquire_gpu(&S->version);
+      if (lane == 30) aux = ld_relaxed_gpu(&S->yield_every);
+      if (lane == 29) aux = *(volatile uint32_t*)&S->trace_on;
       const uint64_t pub = ((uint64_t)__shfl_sync(0xffffffffu, v.y, 0) << 32) | __shfl_sync(0xffffffffu, v.x, 0);
       tail = shfl64(tail, 24);
       if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
@@ -289,58 +307,73 @@ __device__ __forceinline__ bool fetch(DevState* S, uint32_t w, WorkerHeader* H, 
     }
     ++spins;
     if (lane == 0) {
-      flush_mirror(S, w, mir, H->claimed, *(volatile uint64_t*)&H->done);  // idle: counts for wait_all / peek
+      flush_mirror(K, w, mir, H->claimed, *(volatile uint64_t*)&H->done);  // idle: counts for wait_all / peek
       if ((spins & 15) == 0) {
         const uint64_t cur = ld_acquire_gpu(&S->version);
-        if (cur != my_epoch) my_epoch = stable_snapshot(S, w, cur);
-        if (spins == S->spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
+        if (cur != my_epoch) my_epoch = stable_snapshot(S, K, w, cur);
+        if (spins == K.spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
       }
     }
     if (!near) {
       __nanosleep(64u << expn);
-      if (expn < S->backoff_max_exp) ++expn;
+      if (expn < K.backoff_max_exp) ++expn;
     }
   }
+  // Acquire: order this task's data reads after its publication.  The
+  // fence also invalidates this SM's L1 (CCTL.IVALL), so executor loads can
+  // be ordinary L1-allocating loads in a kernel that never relaunches:
+  // buffers rewritten by the host or by other SMs since an earlier task are
+  // re-read from L2.
+  if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  __syncwarp();
   const uint64_t t_seen = globaltimer();
-  ver = shfl64(ver, 31);
+  // claim the next ticket now: the atomic's round trip overlaps this task
+  // (not while held: a held worker takes no new ticket, gpuos_dev_hold)
+  if (lane == 0) next = *(volatile uint32_t*)&S->hold ? kNoTicket : atomicAdd((unsigned long long*)&S->claim, 1ull);
+  uint64_t ver = shfl64(aux, 31);
+  const uint64_t ye = shfl64(aux, 30);
+  const uint32_t tr = (uint32_t)shfl64(aux, 29);
   // stage the descriptor in shared memory
   if (lane < 24) reinterpret_cast<uint4*>(task)[lane] = v;
   __syncwarp();
   if (lane == 0) {
     // free the slot for the producer's next lap (queue.hpp:248)
-    st_relaxed_sys((uint64_t*)(S->ring + (pos & S->mask)), pos + S->cap);
+    st_relaxed_sys((uint64_t*)(K.ring + (pos & K.mask) * kTaskBytes), pos + K.cap);
     const uint64_t claimed = ++H->claimed;
-    if ((claimed & 15) == 0) flush_mirror(S, w, mir, claimed, *(volatile uint64_t*)&H->done);
-    ctl->t_fenced = globaltimer();
+    if ((claimed & 15) == 0) flush_mirror(K, w, mir, claimed, *(volatile uint64_t*)&H->done);
     ctl->pos = pos;
     ctl->exit = 0;
     ctl->t_ticket = t_ticket;
     ctl->t_seen = t_seen;
+    ctl->yield_every = ye;
+    ctl->trace_on = tr;
     if (task->flags & GPUOS_FLAG_SHUTDOWN) {
       atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)pos);
-      quiesce(S, w);
+      quiesce(K, w);
       my_epoch = kQuiescent;
       ctl->exit = 1;
     } else {
-      if (ver != my_epoch) ver = stable_snapshot(S, w, ver);
+      if (ver != my_epoch) ver = stable_snapshot(S, K, w, ver);
       my_epoch = ver;
-      resolve(S, w, H, task->op_id, ver, my_epoch, ctl);
+      resolve(S, K, w, H, task->op_id, ver, my_epoch, ctl);
       ctl->version = ver;
       ctl->t_deq = globaltimer();
     }
   }
+  next = shfl64(next, 0);
+  __syncwarp();
+  const uint32_t plan = plan_task_warp(task, lane);
+  if (lane == 0) ctl->plan = plan;
   __syncwarp();
   return ctl->exit == 0;
 }
 
-// Completion (runtime.hpp:628-639) by lane 0 of one executor warp, rotating
-// per task so that its gpu-scope fence never waits on a sysmem store the same
-// warp issued just before.  The group barrier orders every executor's output
-// writes before the fence; the release puts them in L2 (where the host's copy
-// engine reads) before the word is posted.
+// Completion (runtime.hpp:628-639) by lane 0 of the completer warp.  The
+// DONE barrier orders every executor's output writes before the fence; the
+// release puts them in L2 (where the host's copy engine reads) before the
+// completion word is posted to host memory.
 __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHeader* H, const gpuos_task* task,
-                                              const SharedCtl* ctl, int code, uint64_t& executed) {
-  const uint64_t t_end = globaltimer();
+                                              const SharedCtl* ctl, int code, uint64_t t_end, uint64_t& executed) {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
   if (task->done_cell) {
     const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
@@ -350,7 +383,7 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHea
   atomicAdd((unsigned long long*)&S->processed, 1ull);
   if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);
   atomicAdd((unsigned long long*)&S->per_op[task->op_id < 256 ? task->op_id : 255], 1ull);
-  if (S->trace_on) {
+  if (ctl->trace_on) {
     const uint64_t ticket = atomicAdd((unsigned long long*)&S->trace_head, 1ull);
     TraceRec* r = &S->trace[ticket % S->trace_cap];
     r->stamp = ticket * 2 + 1;
@@ -365,17 +398,14 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHea
     r->t_seen = ctl->t_seen;
     r->t_done = globaltimer();
     r->pad = ctl->t_fenced;
-    __threadfence();
-    r->stamp = ticket * 2 + 2;
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&r->stamp), "l"(ticket * 2 + 2) : "memory");
   }
   ++executed;
-  const uint64_t ye = ld_relaxed_gpu(&S->yield_every);
+  const uint64_t ye = ctl->yield_every;
   if (ye > 0 && executed % ye == 0) __nanosleep(1000);  // yield_every (executor.hpp:190-193)
 }
 
-// One persistent generation.  Warp 0 runs ahead of the executors by up to
-// kBufs tasks, so the PCIe round trip of the next claim overlaps the body and
-// completion of the current one.
+// One persistent generation.
 extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_kernel(DevState* S) {
   extern __shared__ __align__(128) char smem[];
   WorkerHeader* H = reinterpret_cast<WorkerHeader*>(smem);
@@ -393,16 +423,72 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   __syncthreads();
   if (warp == 0) {
     // ---------------- fetcher ----------------
+    WConst K;
+    K.ring = (const char*)S->ring;
+    K.mask = S->mask;
+    K.cap = S->cap;
+    K.host_tail = S->host_tail;
+    K.host_done = S->host_done;
+    K.host_claimed = S->host_claimed;
+    K.host_epoch = S->host_epoch;
+    K.dev_epoch = S->dev_epoch;
+    K.bank[0] = S->bank[0];
+    K.bank[1] = S->bank[1];
+    K.table_slots = S->table_slots;
+    K.spin_iterations = S->spin_iterations;
+    K.backoff_max_exp = S->backoff_max_exp;
     uint64_t my_epoch = kQuiescent;
     Mirror mir;
     mir.flushed_claimed = H->claimed;
     mir.flushed_done = H->done;
+    uint64_t pos = kNoTicket, t_ticket = 0;
+    uint32_t k = 0;
+    for (;; ++k) {
+      const int b = (int)(k % kBufs);
+      if (k >= kBufs) buf_sync<kBarEmpty, kEmptyCount>(b);
+      if (pos == kNoTicket) {
+        if (lane == 0) {
+          while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
+          pos = atomicAdd((unsigned long long*)&S->claim, 1ull);
+        }
+        pos = shfl64(pos, 0);
+      }
+      t_ticket = globaltimer();  // fetch service starts: ticket in hand, buffer free
+      uint64_t next = 0;
+      const bool more = fetch(S, K, w, H, b, pos, t_ticket, next, my_epoch, mir, lane);
+      buf_arrive<kBarFull, kFullCount>(b);
+      if (!more) break;
+      pos = next;
+    }
+    // drain: wait until the completer released every buffer still in flight
+    // (including the exit marker), then publish the final counts as the
+    // single writer of the host mirrors
+    const uint32_t inflight = k + 1 < (uint32_t)kBufs ? k + 1 : (uint32_t)kBufs;
+    for (uint32_t j = k + 1 - inflight; j <= k; ++j) buf_sync<kBarEmpty, kEmptyCount>((int)(j % kBufs));
+    if (lane == 0) {
+      // a ticket claimed ahead past the sentinel stays unused: the next
+      // generation resumes right after the sentinel (gpuos_dev_start)
+      flush_mirror(K, w, mir, H->claimed, *(volatile uint64_t*)&H->done);
+    }
+    return;
+  }
+  if (warp == kCompleterWarp) {
+    // ---------------- completer ----------------
+    uint64_t executed = 0;
     for (uint32_t k = 0;; ++k) {
       const int b = (int)(k % kBufs);
-      if (k >= kBufs) buf_wait_empty(b);
-      const bool more = fetch(S, w, H, b, my_epoch, mir, lane);
-      buf_mark_full(b);
-      if (!more) return;
+      buf_sync<kBarDone, kDoneCount>(b);
+      const SharedCtl* ctl = &H->ctl[b];
+      if (ctl->exit) {
+        buf_arrive<kBarEmpty, kEmptyCount>(b);
+        return;
+      }
+      if (lane == 0) {
+        const int code = ctl->code;
+        complete_task(S, w, H, &H->task[b], ctl, code, ctl->t_end, executed);
+      }
+      __syncwarp();
+      buf_arrive<kBarEmpty, kEmptyCount>(b);
     }
   }
   // ---------------- executors ----------------
@@ -418,33 +504,30 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   ctx.smem_bytes = (int)dyn - (int)kHeaderBytes;
   ctx.aux = 0;
   ctx.flags = 0;
-  uint64_t executed = 0;
-  const int nexec_warps = kExecThreads / 32;
   for (uint32_t k = 0;; ++k) {
     const int b = (int)(k % kBufs);
-    buf_wait_full(b);
-    const gpuos_task* task = &H->task[b];
-    const SharedCtl* ctl = &H->ctl[b];
+    buf_sync<kBarFull, kFullCount>(b);
+    gpuos_task* task = &H->task[b];
+    SharedCtl* ctl = &H->ctl[b];
     if (ctl->exit) {
-      if (ctx.tid == 0) {
-        // final counts for wait_all and the next generation (the fetcher has
-        // returned, so this thread is the only writer now)
-        st_relaxed_sys(&S->host_claimed[w], H->claimed);
-        st_relaxed_sys(&S->host_done[w], H->done);
-      }
+      buf_arrive<kBarDone, kDoneCount>(b);
       return;
     }
+    const uint64_t t_wake = globaltimer();
     int code = ctl->code;
     if (code == GPUOS_OK) {
       ctx.aux = ctl->aux;
-      ctx.flags = task->flags;
+      ctx.flags = task->flags | ctl->plan;
       const OpFn fn = g_kind_fns[ctl->kind];
       code = fn(task, &ctx);
     }
     bar_sync<1>(kExecThreads);
-    if (lane == 0 && warp == 1 + (int)(k % (uint32_t)nexec_warps)) complete_task(S, w, H, task, ctl, code, executed);
-    __syncwarp();
-    buf_mark_empty(b);
+    if (ctx.tid == 0) {
+      ctl->code = code;
+      ctl->t_fenced = t_wake;
+      ctl->t_end = globaltimer();
+    }
+    buf_arrive<kBarDone, kDoneCount>(b);
   }
 }
 
@@ -474,13 +557,23 @@ __device__ __forceinline__ int body(const gpuos_task* t, const Ctx* c) {
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256, 2) gpuos_task_kernel(const gpuos_task task, uint64_t aux, uint32_t* counter) {
+// (256, 3): <= 80 registers, so a standalone kernel's warps fit the register
+// quadrants an SM has left next to a resident worker CTA (9 warps x 96
+// registers); with 128 registers the launch would wait for the generation
+// to exit.
+__global__ void __launch_bounds__(256, 3) gpuos_task_kernel(const gpuos_task task, uint64_t aux, uint32_t* counter) {
   extern __shared__ __align__(128) char tsmem[];
   char* smem = tsmem;
   gpuos_task* t = reinterpret_cast<gpuos_task*>(smem);
   const uint32_t* src = reinterpret_cast<const uint32_t*>(&task);
   for (int i = threadIdx.x; i < (int)(sizeof(gpuos_task) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(t)[i] = src[i];
+  uint32_t* plan_s = reinterpret_cast<uint32_t*>(smem + kTaskBytes);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const uint32_t plan = plan_task_warp(t, threadIdx.x);
+    if (threadIdx.x == 0) *plan_s = plan;
+  }
   __syncthreads();
   uint32_t dyn;
   asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
@@ -493,7 +586,7 @@ __global__ void __launch_bounds__(256, 2) gpuos_task_kernel(const gpuos_task tas
   ctx.smem = smem + kTaskBytes + kCtlBytes;
   ctx.smem_bytes = (int)dyn - (int)(kTaskBytes + kCtlBytes);
   ctx.aux = aux;
-  ctx.flags = t->flags;
+  ctx.flags = t->flags | *plan_s;
   const int code = body<KIND>(t, &ctx);
   __syncthreads();
   if (threadIdx.x == 0 && t->done_cell) {
@@ -537,6 +630,8 @@ static TaskKernel task_kernel_for(uint32_t kind) {
 }
 
 uint32_t worker_smem_bytes() { return kHeaderBytes + kScratchBytes; }
+// standalone task kernels: descriptor + control block + 64 KB scratch
+uint32_t task_smem_bytes() { return kTaskBytes + kCtlBytes + 64 * 1024; }
 uint32_t worker_threads() { return kWorkerThreads; }
 
 // Lazy module loading blocks while the persistent kernel is resident
@@ -545,6 +640,10 @@ uint32_t worker_threads() { return kWorkerThreads; }
 void load_all_kernels(int* worker_regs, size_t* worker_local) {
   const uint32_t smem = worker_smem_bytes();
   cudaFuncSetAttribute(gpuos_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // every kernel asks for the largest shared carveout, so an SM configured by
+  // the resident worker also has room for a standalone task kernel
+  cudaFuncSetAttribute(gpuos_worker_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, gpuos_worker_kernel);
   if (worker_regs) *worker_regs = fa.numRegs;
@@ -552,7 +651,8 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
   const uint32_t kinds[] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, GPUOS_KIND_PROGRAM, GPUOS_KIND_KILLED};
   for (uint32_t k : kinds) {
     TaskKernel f = task_kernel_for(k);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, task_smem_bytes());
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncGetAttributes(&fa, f);
   }
   cudaFuncGetAttributes(&fa, gpuos_clock_probe);
@@ -571,7 +671,7 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
                         cudaStream_t st) {
   TaskKernel f = task_kernel_for(kind);
   void* args[] = {(void*)t, &aux, &counter};
-  return cudaLaunchKernel((const void*)f, dim3(nparts), dim3(256), args, worker_smem_bytes(), st);
+  return cudaLaunchKernel((const void*)f, dim3(nparts), dim3(256), args, task_smem_bytes(), st);
 }
 
 cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st) {

@@ -18,7 +18,7 @@ def summarize(name, ph, t_host=None):
     d = {
         "enq->seen": a[:, 2] - a[:, 0],
         "seen->deq": a[:, 3] - a[:, 2],
-        "seen->fenced": np.array([p.reserved for p in ph], dtype=np.float64),
+        "deq->wake": np.array([p.reserved for p in ph], dtype=np.float64),
         "deq->end(exec)": a[:, 4] - a[:, 3],
         "end->done": a[:, 5] - a[:, 4],
         "ticket->seen": a[:, 2] - a[:, 1],

@@ -6,6 +6,7 @@
 // device-side capacity with no host producer in the loop.
 #include <gpuos/runtime.hpp>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -18,7 +19,9 @@ int main(int argc, char** argv) {
   const int reps = argc > 3 ? std::atoi(argv[3]) : 1;
   RuntimeConfig cfg;
   cfg.capacity = static_cast<size_t>(n) + 2;
-  cfg.telemetry_enabled = false;
+  const bool trace = std::getenv("PROFILE_TRACE") != nullptr;
+  cfg.telemetry_enabled = trace;
+  cfg.trace_capacity = static_cast<size_t>(n) + 16;
   Runtime rt(cfg);
   const int64_t total = int64_t(n) * e;
   TensorView A = rt.alloc_tensor(DType::F32, {total});
@@ -53,6 +56,34 @@ int main(int argc, char** argv) {
     const double bytes = double(n) * e * 12.0;
     std::printf("{\"tasks\": %d, \"elems\": %d, \"kernel_ms\": %.4f, \"tasks_per_s\": %.1f, \"alg_GBps\": %.1f}\n", n, e,
                 ms, n / (ms / 1e3), bytes / (ms / 1e3) / 1e9);
+    if (trace) {
+      std::vector<gpuos_trace_phase> ph(static_cast<size_t>(n));
+      uint64_t got = 0;
+      gpuos_trace_phases(rt.device(), ph.data(), ph.size(), &got);
+      auto pct = [&](auto f, double q) {
+        std::vector<double> v;
+        for (uint64_t i = 0; i < got; ++i) v.push_back(f(ph[i]));
+        std::sort(v.begin(), v.end());
+        return v.empty() ? 0.0 : v[static_cast<size_t>(q * (v.size() - 1))];
+      };
+      auto show = [&](const char* name, auto f) {
+        std::printf("  %-20s p10 %7.2f p50 %7.2f p90 %7.2f us\n", name, pct(f, .1), pct(f, .5), pct(f, .9));
+      };
+      show("fetch(poll..staged)", [](const gpuos_trace_phase& p) { return (double)(int64_t)(p.dequeue_ns - p.ticket_ns) / 1e3; });
+      show("  poll..seen", [](const gpuos_trace_phase& p) { return (double)(int64_t)(p.seen_ns - p.ticket_ns) / 1e3; });
+      show("queue(staged..wake)", [](const gpuos_trace_phase& p) { return p.reserved / 1e3; });
+      show("exec(wake..end)", [](const gpuos_trace_phase& p) { return (double)(int64_t)(p.end_ns - p.dequeue_ns) / 1e3 - p.reserved / 1e3; });
+      show("complete(end..done)", [](const gpuos_trace_phase& p) { return (double)(int64_t)(p.done_ns - p.end_ns) / 1e3; });
+      // per-worker spacing between consecutive tickets (claim cadence)
+      std::vector<double> gaps;
+      std::vector<gpuos_trace_phase> v(ph.begin(), ph.begin() + static_cast<long>(got));
+      std::sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.worker != b.worker ? a.worker < b.worker : a.ticket_ns < b.ticket_ns; });
+      for (size_t i = 1; i < v.size(); ++i)
+        if (v[i].worker == v[i - 1].worker) gaps.push_back((double)(int64_t)(v[i].ticket_ns - v[i - 1].ticket_ns) / 1e3);
+      std::sort(gaps.begin(), gaps.end());
+      if (!gaps.empty())
+        std::printf("  ticket gap per worker p50 %.2f us p90 %.2f us\n", gaps[gaps.size() / 2], gaps[gaps.size() * 9 / 10]);
+    }
   }
   std::vector<float> got(total);
   rt.pool().download(Cv.buffer, got.data(), total * 4);
