@@ -17,6 +17,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -28,6 +29,7 @@
 
 #include "dev_common.cuh"
 #include "dev_state.h"
+#include "ring_format.h"
 #include "gpuos_cuda.h"
 
 using gdev::DevState;
@@ -62,7 +64,8 @@ struct gpuos_dev {
   DevState* S = nullptr;
   DevState shadow{};
   // ring + control words (mapped pinned)
-  char* ring = nullptr;
+  char* ring = nullptr;  // cap x kRingSlot
+  char* ext = nullptr;   // cap x kExtBytes (extended descriptors' views)
   uint64_t* ctl = nullptr;  // [0] tail, then done[W], claimed[W], epoch[W] (each array 128-aligned)
   uint64_t* tail = nullptr;
   uint64_t* mir_done = nullptr;
@@ -291,11 +294,16 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   d->mir_epoch = d->mir_claimed + mir_words;
   for (size_t i = 0; i < W; ++i) d->mir_epoch[i] = gdev::kQuiescent;
   void* ring = nullptr;
-  GPUOS_CK(cudaHostAlloc(&ring, cap * GPUOS_SLOT_BYTES, cudaHostAllocMapped | cudaHostAllocPortable));
-  std::memset(ring, 0, cap * GPUOS_SLOT_BYTES);
+  GPUOS_CK(cudaHostAlloc(&ring, cap * gdev::kRingSlot, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(ring, 0, cap * gdev::kRingSlot);
   d->pinned_blocks.push_back(ring);
   d->ring = (char*)ring;
-  for (uint64_t i = 0; i < cap; ++i) *(uint64_t*)(d->ring + i * GPUOS_SLOT_BYTES) = i;  // slot i free for lap 0
+  for (uint64_t i = 0; i < cap; ++i) *(uint64_t*)(d->ring + i * gdev::kRingSlot) = i;  // slot i free for lap 0
+  void* ext = nullptr;
+  GPUOS_CK(cudaHostAlloc(&ext, cap * gdev::kExtBytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(ext, 0, cap * gdev::kExtBytes);
+  d->pinned_blocks.push_back(ext);
+  d->ext = (char*)ext;
 
   // device state
   GPUOS_CK(cudaMalloc(&d->S, sizeof(DevState)));
@@ -328,7 +336,9 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   s.num_workers = d->workers;
   void* dp = nullptr;
   GPUOS_CK(cudaHostGetDevicePointer(&dp, ring, 0));
-  s.ring = (gpuos_task*)dp;
+  s.ring = (const char*)dp;
+  GPUOS_CK(cudaHostGetDevicePointer(&dp, ext, 0));
+  s.ext = (const char*)dp;
   s.cap = cap;
   s.mask = cap - 1;
   GPUOS_CK(cudaHostGetDevicePointer(&dp, ctl, 0));
@@ -665,37 +675,88 @@ int gpuos_ring_capacity(gpuos_dev* d, uint64_t* c) {
 
 int gpuos_ring_reserve(gpuos_dev* d, uint64_t* pos) {
   const uint64_t p = d->reserve;
-  const uint64_t* w = (const uint64_t*)(d->ring + (p & d->mask) * GPUOS_SLOT_BYTES);
+  const uint64_t* w = (const uint64_t*)(d->ring + (p & d->mask) * gdev::kRingSlot);
   if (__atomic_load_n(w, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
   d->reserve = p + 1;
   *pos = p;
   // The device freed upcoming slots over PCIe, which invalidated their first
   // line in the host caches: fetch it for writing well ahead of use.
-  const char* ahead = d->ring + ((p + 16) & d->mask) * GPUOS_SLOT_BYTES;
+  const char* ahead = d->ring + ((p + 16) & d->mask) * gdev::kRingSlot;
   asm volatile("prefetchw (%0)" ::"r"(ahead));
   return GPUOS_OK;
 }
 
+// Compact encoding (ring_format.h) when every operand is a clean dense view
+// of the output's dtype and shape and at most one scalar is set.
+static bool encode_compact(const gpuos_task* t, uint64_t* w) {
+  if (t->n_inputs > GPUOS_MAX_INPUTS || t->n_scalars > 1 || t->aux != 0) return false;
+  for (int i = 1; i < GPUOS_MAX_SCALARS; ++i)
+    if (t->scalars[i] != 0.0 || std::signbit(t->scalars[i])) return false;
+  if (t->reserved2[0] != 0 || t->reserved2[1] != 0) return false;
+  const gpuos_view& o = t->views[0];
+  if (o.rank > GPUOS_MAX_RANK) return false;
+  int32_t cst[4];
+  gdev::contiguous_strides4(o.extents, o.rank, cst);
+  for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) {
+    const gpuos_view& v = t->views[k];
+    if (k > t->n_inputs) {  // unused views must be all-zero (they expand to zero)
+      static const gpuos_view zero{};
+      if (std::memcmp(&v, &zero, sizeof(v)) != 0) return false;
+      continue;
+    }
+    if (v.status != GPUOS_VIEW_OK || v.dtype != o.dtype || v.rank != o.rank || v.reserved != 0) return false;
+    for (int d = 0; d < GPUOS_MAX_RANK; ++d) {
+      const int32_t want_st = d < o.rank ? cst[d] : 0;
+      if (v.extents[d] != (d < o.rank ? o.extents[d] : 0) || v.strides[d] != want_st) return false;
+    }
+  }
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(t);
+  w[1] = src[1];
+  w[2] = src[2];
+  w[3] = src[3];
+  w[4] = src[4];
+  w[5] = src[5];
+  w[6] = gdev::kFmtCompact | ((uint64_t)o.dtype << 8) | ((uint64_t)o.rank << 16);
+  uint32_t e[4];
+  for (int d = 0; d < 4; ++d) e[d] = (uint32_t)o.extents[d];
+  w[8] = (uint64_t)e[0] | ((uint64_t)e[1] << 32);
+  w[9] = (uint64_t)e[2] | ((uint64_t)e[3] << 32);
+  for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) w[10 + k] = k <= t->n_inputs ? t->views[k].addr : 0;
+  uint64_t s0;
+  std::memcpy(&s0, &t->scalars[0], 8);
+  w[15] = s0;
+  return true;
+}
+
 // Ordinary write-back stores, publication word last.  x86 stores become
 // visible in program order (TSO), also to the device's coherent PCIe reads,
-// so a reader that sees word 0 == pos+1 sees a payload at least that new;
-// a warp-wide read can still interleave with the writes chunk by chunk,
-// which the checksum catches (the device re-reads).  No fence: an sfence
-// per slot (streaming stores) measured ~200 ns, profiles/r01_ring_store.log.
+// so a reader that sees word 0 == pos+1 sees a payload (and an extension
+// record) at least that new; a warp-wide read can still interleave with the
+// writes chunk by chunk, which the checksums catch (the device re-reads).
+// No fence: an sfence per slot (streaming stores) measured ~200 ns.
 int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
   const uint64_t* src = reinterpret_cast<const uint64_t*>(task);
-  uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (pos & d->mask) * GPUOS_SLOT_BYTES);
-  uint64_t h = gdev::slot_term(pos + 1, 0);
-  for (uint32_t i = 1; i < 7; ++i) {
-    uint64_t v = src[i];
-    if (i == 5 && d->shadow.trace_on) v = __rdtsc();  // enqueue stamp, converted at trace export
-    dst[i] = v;
-    h += gdev::slot_term(v, i);
+  uint64_t w[gdev::kSlotWords];
+  if (!encode_compact(task, w)) {
+    // extension record first: views (task words 16..46), checksum bound to pos
+    uint64_t* xd = reinterpret_cast<uint64_t*>(d->ext + (pos & d->mask) * gdev::kExtBytes);
+    uint64_t xh = gdev::ring_term(pos + 1, gdev::kExtChecksumSalt);
+    for (uint32_t i = 0; i + 1 < gdev::kExtWords; ++i) {
+      const uint64_t v = src[16 + i];
+      xd[i] = v;
+      xh += gdev::ring_term(v, i);
+    }
+    xd[gdev::kExtWords - 1] = xh;
+    for (uint32_t i = 1; i < gdev::kSlotWords; ++i) w[i] = src[i];
+    w[6] = gdev::kFmtExtended;  // gpuos_task.aux is reserved (0)
   }
-  for (uint32_t i = 8; i < GPUOS_SLOT_BYTES / 8; ++i) {
-    const uint64_t v = src[i];
-    dst[i] = v;
-    h += gdev::slot_term(v, i);
+  if (d->shadow.trace_on) w[5] = __rdtsc();  // enqueue stamp, converted at trace export
+  uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (pos & d->mask) * gdev::kRingSlot);
+  uint64_t h = gdev::ring_term(pos + 1, 0);
+  for (uint32_t i = 1; i < gdev::kSlotWords; ++i) {
+    if (i == 7) continue;
+    dst[i] = w[i];
+    h += gdev::ring_term(w[i], i);
   }
   dst[7] = h;
   __atomic_store_n(&dst[0], pos + 1, __ATOMIC_RELEASE);
@@ -732,7 +793,7 @@ int gpuos_dev_debug(gpuos_dev* d, char* buf, size_t cap) {
   // slot publication words around the claim window
   std::string slots;
   for (uint64_t p = (tail > 4 ? tail - 4 : 0); p < tail + 4; ++p) {
-    const uint64_t w = *(volatile uint64_t*)(d->ring + (p & d->mask) * GPUOS_SLOT_BYTES);
+    const uint64_t w = *(volatile uint64_t*)(d->ring + (p & d->mask) * gdev::kRingSlot);
     slots += std::to_string(p) + ":" + std::to_string(w) + " ";
   }
   std::snprintf(buf, cap,

@@ -31,10 +31,10 @@ struct Ctx {
 
 typedef int (*OpFn)(const gpuos_task* t, const Ctx* c);
 
-// Task bodies synchronise their worker group on named barrier 1 (barrier 0
-// is the worker loop's __syncthreads).
+// Task bodies synchronise their worker group on its own named barrier
+// (Ctx::bar_id; barrier 0 is the whole CTA).
 __device__ __forceinline__ void group_sync(const Ctx* c) {
-  asm volatile("bar.sync 1, %0;" ::"r"(c->nthreads) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(c->bar_id), "r"(c->nthreads) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -103,6 +103,13 @@ __host__ __device__ __forceinline__ uint64_t slot_term(uint64_t w, uint32_t i) {
 // ---------------------------------------------------------------------------
 // dtype traits.  load() widens to double exactly; narrow() is the single
 // rounding a BoundView::store performs (tensor.hpp:354-371).
+//
+// Coherence rule of the persistent worker: every read of task operand memory
+// is an L2 load (gload / load_any / ld_cg_v4: ld.global.cg).  The kernel never
+// relaunches, so this SM's L1 may hold lines from earlier tasks that other SMs
+// or the host's copy engine have since rewritten; L2 is the coherence point
+// (writers release to L2 before their completion is posted).  load() is for
+// values already in registers.
 // ---------------------------------------------------------------------------
 // static_cast<int32_t>(double) on x86 (cvttsd2si): truncation toward zero,
 // INT32_MIN for NaN or out of range.  GPU cvt.rzi saturates, so
@@ -118,6 +125,7 @@ template <>
 struct DT_<GPUOS_F32> {
   typedef float T;
   static __device__ __forceinline__ double load(const T* p) { return (double)*p; }
+  static __device__ __forceinline__ double gload(const T* p) { return (double)__ldcg(p); }
   static __device__ __forceinline__ void store(T* p, double v) { *p = __double2float_rn(v); }
   static __device__ __forceinline__ double narrow(double v) { return (double)__double2float_rn(v); }
 };
@@ -125,6 +133,7 @@ template <>
 struct DT_<GPUOS_F64> {
   typedef double T;
   static __device__ __forceinline__ double load(const T* p) { return *p; }
+  static __device__ __forceinline__ double gload(const T* p) { return __ldcg(p); }
   static __device__ __forceinline__ void store(T* p, double v) { *p = v; }
   static __device__ __forceinline__ double narrow(double v) { return v; }
 };
@@ -132,6 +141,7 @@ template <>
 struct DT_<GPUOS_I32> {
   typedef int32_t T;
   static __device__ __forceinline__ double load(const T* p) { return (double)*p; }
+  static __device__ __forceinline__ double gload(const T* p) { return (double)__ldcg(p); }
   static __device__ __forceinline__ void store(T* p, double v) { *p = narrow_i32(v); }
   static __device__ __forceinline__ double narrow(double v) { return (double)narrow_i32(v); }
 };
@@ -139,6 +149,7 @@ template <>
 struct DT_<GPUOS_F16> {
   typedef __half T;
   static __device__ __forceinline__ double load(const T* p) { return (double)__half2float(*p); }
+  static __device__ __forceinline__ double gload(const T* p) { return (double)__half2float(__ldcg(p)); }
   static __device__ __forceinline__ void store(T* p, double v) { *p = __double2half(v); }
   static __device__ __forceinline__ double narrow(double v) { return (double)__half2float(__double2half(v)); }
 };
@@ -146,6 +157,7 @@ template <>
 struct DT_<GPUOS_BF16> {
   typedef __nv_bfloat16 T;
   static __device__ __forceinline__ double load(const T* p) { return (double)__bfloat162float(*p); }
+  static __device__ __forceinline__ double gload(const T* p) { return (double)__bfloat162float(__ldcg(p)); }
   static __device__ __forceinline__ void store(T* p, double v) { *p = __double2bfloat16(v); }
   static __device__ __forceinline__ double narrow(double v) {
     return (double)__bfloat162float(__double2bfloat16(v));
@@ -160,11 +172,11 @@ __host__ __device__ __forceinline__ int dtype_width(int dt) {
 // math, e.g. rope/sdpa/matmul staging).
 __device__ __forceinline__ double load_any(int dt, const char* base, int64_t elem) {
   switch (dt) {
-    case GPUOS_F32: return (double)((const float*)base)[elem];
-    case GPUOS_F64: return ((const double*)base)[elem];
-    case GPUOS_I32: return (double)((const int32_t*)base)[elem];
-    case GPUOS_F16: return (double)__half2float(((const __half*)base)[elem]);
-    default: return (double)__bfloat162float(((const __nv_bfloat16*)base)[elem]);
+    case GPUOS_F32: return (double)__ldcg((const float*)base + elem);
+    case GPUOS_F64: return __ldcg((const double*)base + elem);
+    case GPUOS_I32: return (double)__ldcg((const int32_t*)base + elem);
+    case GPUOS_F16: return (double)__half2float(__ldcg((const __half*)base + elem));
+    default: return (double)__bfloat162float(__ldcg((const __nv_bfloat16*)base + elem));
   }
 }
 __device__ __forceinline__ void store_any(int dt, char* base, int64_t elem, double v) {

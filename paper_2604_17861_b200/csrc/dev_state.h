@@ -16,8 +16,8 @@ constexpr uint64_t kRunning = ~0ull;    // stop_pos while running
 constexpr uint32_t kNumKinds = 80;      // module jump-table slots
 constexpr uint32_t kTaskBytes = 384;
 constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
-constexpr uint32_t kHeaderBytes = 4096;  // worker: task buffers, control blocks, counters, entry cache
-constexpr uint32_t kScratchBytes = 92 * 1024;
+constexpr uint32_t kHeaderBytes = 5120;  // worker: task buffers, control blocks, counters, entry cache
+constexpr uint32_t kScratchBytes = 91 * 1024;
 constexpr uint32_t kLaunchCounters = 1u << 16;
 
 // One operator-table entry (optable.hpp:40-48): the device function is named
@@ -84,7 +84,8 @@ struct alignas(128) DevState {
   uint32_t table_slots;
   uint32_t num_workers;
   // task ring in mapped pinned host memory
-  gpuos_task* ring;
+  const char* ring;  // cap x kRingSlot (ring_format.h)
+  const char* ext;   // cap x kExtBytes
   uint64_t cap;
   uint64_t mask;
   const uint64_t* host_tail;  // producer's published count

@@ -98,7 +98,7 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
     for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
       double x[A];
 #pragma unroll
-      for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + e);
+      for (int k = 0; k < A; ++k) x[k] = DT_<DT>::gload(in[k] + e);
       DT_<DT>::store(out + e, f(x));
     }
     return;
@@ -106,7 +106,7 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
   for (int64_t e = tail_lo + c->tid; e < n; e += c->nthreads) {
     double x[A];
 #pragma unroll
-    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + e);
+    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::gload(in[k] + e);
     DT_<DT>::store(out + e, f(x));
   }
 }
@@ -127,7 +127,7 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
     space_offsets(s, (uint32_t)e, off);
     double x[A];
 #pragma unroll
-    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(in[k] + off[1 + k]);
+    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::gload(in[k] + off[1 + k]);
     DT_<DT>::store(out + off[0], f(x));
   }
 }
@@ -291,15 +291,20 @@ __device__ void program_loop(const gpuos_task* t, const Ctx* c, const Space& s, 
       space_offsets(s, (uint32_t)e, off);
     }
     double x[GPUOS_MAX_INPUTS];
-    for (int k = 0; k < arity; ++k) x[k] = DT_<DT>::load(in[k] + off[1 + k]);
+    for (int k = 0; k < arity; ++k) x[k] = DT_<DT>::gload(in[k] + off[1 + k]);
     DT_<DT>::store(out + off[0], run_program(code, n_instr, x));
   }
 }
 
 // Checks in load_module's order (opcompiler.hpp:72-101).
 __device__ __noinline__ int op_program(const gpuos_task* t, const Ctx* c) {
-  const ProgramHeader* h = (const ProgramHeader*)c->aux;
-  if (h == nullptr) return GPUOS_VERIFY_ERROR;
+  const ProgramHeader* hp = (const ProgramHeader*)c->aux;
+  if (hp == nullptr) return GPUOS_VERIFY_ERROR;
+  ProgramHeader hh;  // L2 reads (see the coherence rule in dev_common.cuh)
+  hh.n_instr = __ldcg(&hp->n_instr);
+  hh.arity = __ldcg(&hp->arity);
+  hh.dtype = __ldcg(&hp->dtype);
+  const ProgramHeader* h = &hh;
   const int arity = h->arity;
   if (t->n_inputs != arity) return GPUOS_ARITY_ERROR;
   const gpuos_view& out = t->views[0];
@@ -327,8 +332,8 @@ __device__ __noinline__ int op_program(const gpuos_task* t, const Ctx* c) {
   // stage the program in shared memory (<= GPUOS_MAX_PROGRAM instructions)
   const int n_instr = (int)h->n_instr;
   gpuos_instr* code = (gpuos_instr*)c->smem;
-  const gpuos_instr* src = (const gpuos_instr*)(h + 1);
-  for (int i = c->tid; i < n_instr; i += c->nthreads) code[i] = src[i];
+  const uint4* src = (const uint4*)(hp + 1);
+  for (int i = c->tid; i < n_instr; i += c->nthreads) reinterpret_cast<uint4*>(code)[i] = __ldcg(src + i);
   group_sync(c);
   switch (out.dtype) {
     case GPUOS_F32: program_loop<GPUOS_F32>(t, c, s, n, code, n_instr, arity); break;

@@ -47,22 +47,27 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
   const int64_t so0 = out.strides[0], so1 = out.strides[1];
   double* As = (double*)c->smem;             // [kTM][kTK+1]
   double* Bs = As + kTM * (kTK + 1);         // [kTK][kTN+1]
-  const int ntm = (m + kTM - 1) / kTM, ntn = (n + kTN - 1) / kTN;
+  const int nt = c->nthreads;
+  // Thread grid: (nt/16) x 16 threads, 4x4 outputs each (rows ty + R*r, cols
+  // tx + 16q), so a tile is (4*nt/16) x 64: 64x64 for a 256-thread group,
+  // 32x64 for the worker's 128-thread groups.  Other group sizes use the
+  // element loop with a tile small enough that 16 outputs per thread cover it.
+  const bool grid = (nt % 16 == 0) && nt >= 16 && nt <= 256;
+  const int R = nt / 16;
+  const int TM = grid ? 4 * R : ((nt * 16) / kTN < kTM ? ((nt * 16) / kTN > 0 ? (nt * 16) / kTN : 1) : kTM);
+  const int ntm = (m + TM - 1) / TM, ntn = (n + kTN - 1) / kTN;
   int64_t tlo, thi;
   part_range((int64_t)ntm * ntn, c->part, c->nparts, 1, &tlo, &thi);
-  const int nt = c->nthreads;
-  // 256 threads: 16x16 grid, 4x4 outputs each (rows ty+16r, cols tx+16q)
   const int ty = c->tid >> 4, tx = c->tid & 15;
-  const bool grid16 = (nt == 256);
   for (int64_t tile = tlo; tile < thi; ++tile) {
-    const int i0 = (int)(tile / ntn) * kTM, j0 = (int)(tile % ntn) * kTN;
+    const int i0 = (int)(tile / ntn) * TM, j0 = (int)(tile % ntn) * kTN;
     double acc[4][4];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
     for (int k0 = 0; k0 < k; k0 += kTK) {
-      for (int e = c->tid; e < kTM * kTK; e += nt) {
+      for (int e = c->tid; e < TM * kTK; e += nt) {
         const int i = e / kTK, kk = e % kTK;
         const int gi = i0 + i, gk = k0 + kk;
         As[i * (kTK + 1) + kk] = (gi < m && gk < k) ? load_any(dt, ap, gi * sa0 + gk * sa1) : 0.0;
@@ -74,11 +79,11 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
       }
       group_sync(c);
       const int kmax = (k - k0) < kTK ? (k - k0) : kTK;
-      if (grid16) {
+      if (grid) {
         for (int kk = 0; kk < kmax; ++kk) {
           double av[4], bv[4];
 #pragma unroll
-          for (int r = 0; r < 4; ++r) av[r] = As[(ty + 16 * r) * (kTK + 1) + kk];
+          for (int r = 0; r < 4; ++r) av[r] = As[(ty + R * r) * (kTK + 1) + kk];
 #pragma unroll
           for (int q = 0; q < 4; ++q) bv[q] = Bs[kk * (kTN + 1) + tx + 16 * q];
 #pragma unroll
@@ -87,10 +92,10 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
             for (int q = 0; q < 4; ++q) acc[r][q] = mac(acc[r][q], av[r], bv[q], exact);
         }
       } else {
-        // generic group size: each thread owns tile elements e = tid + nt*s (s < 16)
+        // each thread owns tile elements e = tid + nt*s (s < 16)
         for (int s = 0; s < 16; ++s) {
           const int e = c->tid + nt * s;
-          if (e >= kTM * kTN) break;
+          if (e >= TM * kTN) break;
           const int i = e / kTN, j = e % kTN;
           double v = acc[s >> 2][s & 3];
           for (int kk = 0; kk < kmax; ++kk) v = mac(v, As[i * (kTK + 1) + kk], Bs[kk * (kTN + 1) + j], exact);
@@ -99,18 +104,18 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
       }
       group_sync(c);
     }
-    if (grid16) {
+    if (grid) {
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int gi = i0 + ty + 16 * r, gj = j0 + tx + 16 * q;
+          const int gi = i0 + ty + R * r, gj = j0 + tx + 16 * q;
           if (gi < m && gj < n) store_any(dt, op, gi * so0 + gj * so1, acc[r][q]);
         }
     } else {
       for (int s = 0; s < 16; ++s) {
         const int e = c->tid + nt * s;
-        if (e >= kTM * kTN) break;
+        if (e >= TM * kTN) break;
         const int gi = i0 + e / kTN, gj = j0 + e % kTN;
         if (gi < m && gj < n) store_any(dt, op, gi * so0 + gj * so1, acc[s >> 2][s & 3]);
       }

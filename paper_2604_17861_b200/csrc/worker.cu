@@ -1,27 +1,28 @@
 // The persistent sm_100a worker kernel (reference Executor, executor.hpp:45-278,
-// re-designed as one resident CTA per worker), the module jump table, and the
-// standalone per-task kernels of the conventional path (execute_inline,
-// runtime.hpp:567-619 == baseline (a): one cudaLaunchKernel per task).
+// re-designed as one resident CTA per SM with warp-specialised stages), the
+// module jump table, and the standalone per-task kernels of the conventional
+// path (execute_inline, runtime.hpp:567-619 == baseline (a): one
+// cudaLaunchKernel per task).
 //
-// Claim protocol (queue.hpp:179-261 restated for PCIe):
-//   * warp 0, lane 0 takes a ticket `pos` with atomicAdd on the HBM claim
-//     cursor; tickets are FIFO, so the shutdown sentinel drains all earlier
-//     work (executor.hpp:178-184).
-//   * the warp polls slot pos in mapped pinned memory with one 384-byte
-//     warp-wide volatile load (24 lanes x 16 B) plus the producer tail
-//     (lane 24); publication = slot word 0 == pos+1, torn reads are caught by
-//     a warp-reduced checksum (queue.hpp:249-251).  Only tickets within two
-//     of the highest tail seen on the device poll PCIe continuously; the rest
-//     back off on an HBM hint, so idle PCIe traffic stays small.
-//   * lane 0 frees the slot (word 0 = pos + capacity, queue.hpp:248), mirrors
-//     its claimed count to host memory, snapshots the table version with the
-//     publish-then-revalidate epoch protocol (executor.hpp:133-141), and looks
-//     the op up in the bank of that version with the generation canary
-//     (executor.hpp:197-212).
-//   * all warps run the task body; thread 0 posts the completion word with a
-//     system-scope release and the per-worker processed count.
+// Claim protocol (queue.hpp:179-261 restated for PCIe; ring_format.h):
+//   * the fetcher warp takes tickets with atomicAdd on the HBM claim cursor
+//     (one, or a batch of four under backlog); tickets are FIFO, so the
+//     shutdown sentinel drains all earlier work (executor.hpp:178-184).
+//   * it polls the 128-byte slots in mapped pinned memory with one warp-wide
+//     read; publication = word 0 == pos+1, torn reads fail a checksum
+//     (queue.hpp:249-251); extended descriptors add one read of their
+//     extension record.
+//   * it frees the slot (word 0 = pos + capacity, queue.hpp:248), snapshots the
+//     table version with the publish-then-revalidate epoch protocol
+//     (executor.hpp:133-141), resolves the op in the bank of that version with
+//     the generation canary (executor.hpp:197-212), and hands the task to an
+//     executor group through a shared-memory buffer.
+//   * the executor group calls the body through the device jump table; the
+//     completer warp posts the completion word with a system-scope store
+//     after a gpu-scope release fence, and the per-worker processed count.
 #include "dev_common.cuh"
 #include "dev_state.h"
+#include "ring_format.h"
 #include "ops_elementwise.cuh"
 #include "ops_linalg.cuh"
 #include "ops_rowwise.cuh"
@@ -71,28 +72,31 @@ struct SharedCtl {
 constexpr uint32_t kCtlStride = 112;
 static_assert(sizeof(SharedCtl) <= kCtlStride, "SharedCtl must fit its stride");
 
-// Worker CTA shape (warp-specialised pipeline, one task per buffer):
-//   warp 0      fetcher   : claim ticket -> PCIe slot read -> stage -> resolve
-//   warps 1..8  executors : the task body as one 256-thread group
+// Worker CTA shape (warp-specialised pipeline):
+//   warp 0      fetcher   : claim tickets -> PCIe slot read -> stage -> resolve
+//   warps 1..4  executor group 0 (128 threads)   } two tasks execute at once,
+//   warps 5..8  executor group 1 (128 threads)   } so one SM keeps ~2 tasks of
+//                                                   HBM traffic in flight
 //   warp 9      completer : output fence -> completion word -> counters
-// so the PCIe round trip of the next claim and the completion fence of the
-// previous task both overlap the current body.
-constexpr int kExecThreads = 256;
-constexpr int kWorkerThreads = 32 + kExecThreads + 32;
-constexpr int kCompleterWarp = 1 + kExecThreads / 32;
-constexpr int kBufs = 3;
-// Named barriers: 0 = whole CTA, 1 = executor group (task bodies),
-// FULL[b]  = 2+b : fetcher arrives, executors wait      (32 + 256)
-// DONE[b]  = 5+b : executors arrive, completer waits    (256 + 32)
-// EMPTY[b] = 8+b : completer arrives, fetcher waits     (32 + 32)
-constexpr int kBarFull = 2, kBarDone = 5, kBarEmpty = 8;
-constexpr int kFullCount = 32 + kExecThreads, kDoneCount = kExecThreads + 32, kEmptyCount = 64;
+// Tasks flow through kBufs shared buffers in ticket order: task k uses buffer
+// k % kBufs and executor group k % 2; the completer retires them in order.
+constexpr int kGroups = 2;
+constexpr int kGroupThreads = 128;
+constexpr int kWorkerThreads = 32 + kGroups * kGroupThreads + 32;
+constexpr int kCompleterWarp = 1 + kGroups * kGroupThreads / 32;
+constexpr int kBufs = 4;
+// Named barriers: 0 = whole CTA, 1+g = executor group g (task bodies),
+// FULL[b]  = 3+b  : fetcher arrives, group waits      (32 + 128)
+// DONE[b]  = 7+b  : group arrives, completer waits    (128 + 32)
+// EMPTY[b] = 11+b : completer arrives, fetcher waits  (32 + 32)
+constexpr int kBarFull = 3, kBarDone = 7, kBarEmpty = 11;
+constexpr int kFullCount = 32 + kGroupThreads, kDoneCount = kGroupThreads + 32, kEmptyCount = 64;
+constexpr int kMaxBatch = 4;  // tickets claimed per atomic / slots per warp-wide read
 // Per-CTA cache of resolved table entries, tagged with the version they were
 // resolved under: an entry of version v is immutable while v is current
 // (the host rewrites a bank only after every epoch moved past it), so a tag
 // hit needs no HBM lookup.
 constexpr int kEntryCache = 64;
-constexpr uint64_t kNoTicket = ~0ull;
 struct CachedEntry {
   uint64_t version;  // kQuiescent = invalid
   uint64_t aux;
@@ -103,18 +107,19 @@ struct CachedEntry {
 };
 static_assert(sizeof(CachedEntry) == 32, "cache entry is 32 bytes");
 
-// Shared header (kHeaderBytes): tasks | ctls | counters | entry cache.
+// Shared header (kHeaderBytes): tasks | ctls | raw slot staging | counters | entry cache.
 struct WorkerHeader {
   gpuos_task task[kBufs];
   SharedCtl ctl[kBufs];
-  uint64_t done;     // tasks completed by this CTA (all generations)
-  uint64_t claimed;  // tickets claimed by this CTA (all generations)
-  uint64_t pad[2];
+  uint64_t raw[kMaxBatch][kSlotWords];  // slots as read, before expansion
+  uint64_t done;                        // tasks completed by this CTA (all generations)
+  uint64_t claimed;                     // tickets claimed by this CTA (all generations)
   CachedEntry cache[kEntryCache];
 };
 static_assert(sizeof(WorkerHeader) <= kHeaderBytes, "worker header overflows");
 
-// Barrier ids must be immediates (a register id makes ptxas reserve all 16).
+// Barrier ids must be immediates where possible (a register id makes ptxas
+// reserve all 16); the per-buffer families dispatch over constants.
 template <int ID>
 __device__ __forceinline__ void bar_sync(int n) {
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
@@ -125,16 +130,23 @@ __device__ __forceinline__ void bar_arrive(int n) {
 }
 template <int BASE, int N>
 __device__ __forceinline__ void buf_sync(int b) {
-  if (b == 0) bar_sync<BASE>(N);
-  else if (b == 1) bar_sync<BASE + 1>(N);
-  else bar_sync<BASE + 2>(N);
+  switch (b) {
+    case 0: bar_sync<BASE>(N); break;
+    case 1: bar_sync<BASE + 1>(N); break;
+    case 2: bar_sync<BASE + 2>(N); break;
+    default: bar_sync<BASE + 3>(N); break;
+  }
 }
 template <int BASE, int N>
 __device__ __forceinline__ void buf_arrive(int b) {
-  if (b == 0) bar_arrive<BASE>(N);
-  else if (b == 1) bar_arrive<BASE + 1>(N);
-  else bar_arrive<BASE + 2>(N);
+  switch (b) {
+    case 0: bar_arrive<BASE>(N); break;
+    case 1: bar_arrive<BASE + 1>(N); break;
+    case 2: bar_arrive<BASE + 2>(N); break;
+    default: bar_arrive<BASE + 3>(N); break;
+  }
 }
+static_assert(kBufs == 4, "buf_sync/buf_arrive dispatch four buffers");
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
@@ -143,6 +155,7 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
 // Constant per generation: read once from DevState at kernel start.
 struct WConst {
   const char* ring;
+  const char* ext;
   uint64_t mask, cap;
   const uint64_t* host_tail;
   uint64_t* host_done;
@@ -150,7 +163,7 @@ struct WConst {
   uint64_t* host_epoch;
   uint64_t* dev_epoch;
   TableEntry* bank[2];
-  uint32_t table_slots, spin_iterations, backoff_max_exp;
+  uint32_t table_slots, spin_iterations, backoff_max_exp, num_workers;
 };
 
 // Publish-then-revalidate (executor.hpp:133-141): the epoch slot holds the
@@ -243,129 +256,292 @@ __device__ __forceinline__ void resolve(DevState* S, const WConst& K, uint32_t w
   ce->aux = e.aux;
 }
 
-// Fetcher: wait for ticket `pos`'s publication, stage the slot in buffer
-// `b`, free the slot, resolve the op.  `next` is the ticket claimed ahead for
-// the following call.  Returns false at the sentinel (or past the stop
-// position), with ctl->exit set.
-//
-// PCIe discipline (measured, profiles/r01_phases_*.log): every host-memory
-// access costs a round trip through the PCIe path and a fence that follows a
-// sysmem store waits for it, so this path issues one slot read (the version
-// and the live knobs ride along on lanes 25..31), one slot-free store, the
-// tail read only when the ticket is past the hint, and one gpu-scope acquire
-// fence once the slot validated (it invalidates this SM's L1 for the task).
-__device__ __forceinline__ bool fetch(DevState* S, const WConst& K, uint32_t w, WorkerHeader* H, int b,
-                                      uint64_t pos, uint64_t t_ticket, uint64_t& next, uint64_t& my_epoch,
-                                      Mirror& mir, int lane) {
-  gpuos_task* task = &H->task[b];
-  SharedCtl* ctl = &H->ctl[b];
-  const char* slot = K.ring + (pos & K.mask) * kTaskBytes;
-  uint32_t spins = 0, expn = 0;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  uint64_t aux = 0;  // lane 31: version, lane 30: yield_every, lane 29: trace_on
+// Expand a staged compact slot into the ABI descriptor: lane L (< 24) writes
+// task words 2L and 2L+1, exactly the words the host's build_task produced.
+__device__ __forceinline__ void expand_compact(const uint64_t* raw, gpuos_task* task, int lane) {
+  if (lane >= 24) return;
+  uint64_t out[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int wi = 2 * lane + h;
+    uint64_t v = 0;
+    if (wi < 6) {
+      v = raw[wi];
+    } else if (wi == 7) {
+      v = raw[7];
+    } else if (wi == 8) {
+      v = raw[15];  // scalars[0]
+    } else if (wi >= 16 && wi < 46) {
+      const int k = (wi - 16) / 6, f = (wi - 16) % 6;
+      const uint32_t n_inputs = (uint32_t)((raw[2] >> 48) & 0xff);
+      if ((uint32_t)k <= n_inputs) {
+        const uint32_t dtype = (uint32_t)((raw[6] >> 8) & 0xff), rank = (uint32_t)((raw[6] >> 16) & 0xff);
+        int32_t ext[4] = {(int32_t)(uint32_t)raw[8], (int32_t)(uint32_t)(raw[8] >> 32), (int32_t)(uint32_t)raw[9],
+                          (int32_t)(uint32_t)(raw[9] >> 32)};
+        int32_t st[4];
+        contiguous_strides4(ext, (int)rank, st);
+        switch (f) {
+          case 0: v = raw[10 + k]; break;                                         // addr
+          case 1: v = raw[8]; break;                                              // extents 0,1
+          case 2: v = raw[9]; break;                                              // extents 2,3
+          case 3: v = (uint64_t)(uint32_t)st[0] | ((uint64_t)(uint32_t)st[1] << 32); break;
+          case 4: v = (uint64_t)(uint32_t)st[2] | ((uint64_t)(uint32_t)st[3] << 32); break;
+          default: v = (uint64_t)dtype | ((uint64_t)rank << 8); break;            // status 0, buffer_lo 0
+        }
+      }
+    }
+    out[h] = v;
+  }
+  reinterpret_cast<uint4*>(task)[lane] =
+      make_uint4((uint32_t)out[0], (uint32_t)(out[0] >> 32), (uint32_t)out[1], (uint32_t)(out[1] >> 32));
+}
+
+// Stage the extension record of an extended slot (task words 16..46): one
+// 256-byte read by lanes 0..15, validated against its position-bound checksum.
+__device__ __forceinline__ void fetch_ext(DevState* S, const WConst& K, uint64_t pos, gpuos_task* task, int lane) {
+  const char* rec = K.ext + (pos & K.mask) * kExtBytes;
   for (;;) {
-    const uint64_t sp = ld_relaxed_gpu(&S->stop_pos);
-    if (pos > sp) {
-      if (lane == 0) {
-        quiesce(K, w);
-        my_epoch = kQuiescent;
-        ctl->exit = 1;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (lane < 16) v = ld_volatile_v4(rec + 16 * lane);
+    const uint64_t w0 = ((uint64_t)v.y << 32) | v.x, w1 = ((uint64_t)v.w << 32) | v.z;
+    uint64_t part = 0;
+    if (lane < 16) {
+      part = ring_term(w0, 2 * lane);
+      if (lane != 15) part += ring_term(w1, 2 * lane + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    part += ring_term(pos + 1, kExtChecksumSalt);
+    const uint64_t chk = shfl64(w1, 15);
+    if (part == chk) {
+      if (lane < 16) {
+        if (lane == 15) v.z = v.w = 0;  // reserved2[1] carried the checksum
+        reinterpret_cast<uint4*>(task)[8 + lane] = v;
       }
       __syncwarp();
-      return false;
+      return;
     }
-    // Only tickets within two of the highest tail seen on the device read
-    // PCIe; the rest watch the HBM hint.  Progress: the ticket equal to the
-    // hint is always near, and its poll carries the producer tail (lane 24),
-    // so every publication eventually advances the hint.
-    const uint64_t h = ld_relaxed_gpu(&S->hint);
-    const bool near = pos < h + 2;
-    if (near) {
-      if (lane < 24) v = ld_volatile_v4(slot + 16 * lane);
-      uint64_t tail = 0;
-      if (lane == 24 && pos >= h) tail = ld_relaxed_sys(K.host_tail);
-      if (lane == 31) aux = ld_acquire_gpu(&S->version);
-      if (lane == 30) aux = ld_relaxed_gpu(&S->yield_every);
-      if (lane == 29) aux = *(volatile uint32_t*)&S->trace_on;
-      const uint64_t pub = ((uint64_t)__shfl_sync(0xffffffffu, v.y, 0) << 32) | __shfl_sync(0xffffffffu, v.x, 0);
-      tail = shfl64(tail, 24);
-      if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
-      if (pub == pos + 1) {
-        const uint64_t w0 = ((uint64_t)v.y << 32) | v.x, w1 = ((uint64_t)v.w << 32) | v.z;
-        uint64_t part = 0;
-        if (lane < 24) {
-          part = slot_term(w0, 2 * lane);
-          if (lane != 3) part += slot_term(w1, 2 * lane + 1);  // word 7 is the checksum
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        const uint64_t chk = shfl64(w1, 3);
-        if (part == chk) break;
-        if (lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
-        continue;  // torn: re-read immediately
-      }
-    }
-    ++spins;
+    if (lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
+  }
+}
+
+// Shared state of the fetcher warp (registers, uniform across the warp).
+struct Fetcher {
+  uint64_t my_epoch = kQuiescent;
+  Mirror mir;
+  uint32_t k = 0;  // tasks (and exit markers) handed to the executors so far
+};
+
+// Hand the next buffer to the executors: wait until the completer released
+// it (after its first lap), return its index.
+__device__ __forceinline__ int next_buffer(Fetcher& F) {
+  const int b = (int)(F.k % kBufs);
+  if (F.k >= (uint32_t)kBufs) buf_sync<kBarEmpty, kEmptyCount>(b);
+  return b;
+}
+
+// Exit: one marker per executor group (each waits on its own buffers), then
+// wait for the completer to release everything in flight, then publish the
+// final counts as the single writer of the host mirrors.
+__device__ __forceinline__ void fetcher_exit(const WConst& K, uint32_t w, WorkerHeader* H, Fetcher& F, int lane,
+                                             bool first_marker_staged) {
+  for (int g = first_marker_staged ? 1 : 0; g < kGroups; ++g) {
+    const int b = next_buffer(F);
+    if (lane == 0) H->ctl[b].exit = 1;
+    __syncwarp();
+    buf_arrive<kBarFull, kFullCount>(b);
+    ++F.k;
+  }
+  const uint32_t inflight = F.k < (uint32_t)kBufs ? F.k : (uint32_t)kBufs;
+  for (uint32_t q = F.k - inflight; q < F.k; ++q) buf_sync<kBarEmpty, kEmptyCount>((int)(q % kBufs));
+  if (lane == 0) flush_mirror(K, w, F.mir, H->claimed, *(volatile uint64_t*)&H->done);
+}
+
+// The fetcher warp's whole life.
+//
+// Claim: one atomicAdd takes 1 ticket, or kMaxBatch when the device-visible
+// tail shows a backlog of more than two tickets per worker (batching then
+// costs no latency and cuts PCIe round trips per task by up to 4x).
+// Poll: lanes 8j..8j+7 read slot j of the batch (one warp-wide 512-byte read);
+// publication = word 0 == pos+1, torn reads fail the slot checksum.  Only
+// tickets within two of the highest tail seen on the device read PCIe; the
+// rest watch the HBM hint.  Progress: the ticket equal to the hint is always
+// near, and its poll carries the producer tail, so every publication
+// eventually advances the hint.
+__device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint32_t w, int lane) {
+  WConst K;
+  K.ring = S->ring;
+  K.ext = S->ext;
+  K.mask = S->mask;
+  K.cap = S->cap;
+  K.host_tail = S->host_tail;
+  K.host_done = S->host_done;
+  K.host_claimed = S->host_claimed;
+  K.host_epoch = S->host_epoch;
+  K.dev_epoch = S->dev_epoch;
+  K.bank[0] = S->bank[0];
+  K.bank[1] = S->bank[1];
+  K.table_slots = S->table_slots;
+  K.spin_iterations = S->spin_iterations;
+  K.backoff_max_exp = S->backoff_max_exp;
+  K.num_workers = S->num_workers;
+  Fetcher F;
+  F.mir.flushed_claimed = H->claimed;
+  F.mir.flushed_done = H->done;
+  uint64_t last_pos = 0, hint_seen = ld_relaxed_gpu(&S->hint);
+  const int seg = lane >> 3, sl = lane & 7;
+  for (;;) {
+    // ---- claim a batch ----
+    uint64_t pos = 0;
+    uint32_t nb = 1;
     if (lane == 0) {
-      flush_mirror(K, w, mir, H->claimed, *(volatile uint64_t*)&H->done);  // idle: counts for wait_all / peek
-      if ((spins & 15) == 0) {
-        const uint64_t cur = ld_acquire_gpu(&S->version);
-        if (cur != my_epoch) my_epoch = stable_snapshot(S, K, w, cur);
-        if (spins == K.spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
+      while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
+      nb = hint_seen > last_pos + 2ull * K.num_workers ? (uint32_t)kMaxBatch : 1u;
+      pos = atomicAdd((unsigned long long*)&S->claim, (unsigned long long)nb);
+      last_pos = pos + nb - 1;
+    }
+    pos = shfl64(pos, 0);
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    uint32_t j = 0;  // next slot of the batch to hand over
+    const uint64_t t_ticket = globaltimer();
+    uint32_t spins = 0, expn = 0;
+    while (j < nb) {
+      // One round of loads, issued back to back: the slots (near tickets
+      // only), then the control words on single lanes.  All are relaxed: an
+      // acquire would run CCTL.IVALL and drop the executors' L1-resident
+      // stacks.  Table entries are L2 loads issued after the version read
+      // returned, and the host writes a bank before it publishes the version
+      // that selects it, so an entry read under version v sees v's bank.
+      // Nearness uses the hint seen by the previous round.
+      const bool near = pos + j < hint_seen + 2;
+      uint32_t ready = 0;  // consecutive valid slots starting at j
+      uint4 v = make_uint4(0, 0, 0, 0);
+      uint64_t aux = 0;    // lane 1: version, 2: yield_every, 3: trace_on, 4: tail, 5: stop_pos, 6: hint
+      const uint32_t sj = j + (uint32_t)seg;
+      const uint64_t spos = pos + sj;
+      if (near && sj < nb) v = ld_volatile_v4(K.ring + (spos & K.mask) * kRingSlot + 16 * sl);
+      if (near && lane == 4 && pos + nb - 1 >= hint_seen) aux = ld_relaxed_sys(K.host_tail);
+      if (lane == 5) aux = ld_relaxed_gpu(&S->stop_pos);
+      if (lane == 6) aux = ld_relaxed_gpu(&S->hint);
+      if (near && lane == 2) aux = ld_relaxed_gpu(&S->yield_every);
+      if (near && lane == 3) aux = *(volatile uint32_t*)&S->trace_on;
+      if (near && lane == 1) aux = ld_relaxed_gpu(&S->version);
+      const uint64_t sp = shfl64(aux, 5);
+      const uint64_t h = shfl64(aux, 6);
+      const uint64_t tail = near ? shfl64(aux, 4) : 0;
+      if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
+      hint_seen = tail > h ? tail : h;
+      if (pos + j > sp) {
+        if (lane == 0) {
+          quiesce(K, w);
+          F.my_epoch = kQuiescent;
+        }
+        fetcher_exit(K, w, H, F, lane, false);
+        return;
+      }
+      if (near) {
+        const uint64_t w0 = ((uint64_t)v.y << 32) | v.x, w1 = ((uint64_t)v.w << 32) | v.z;
+        uint64_t part = ring_term(w0, 2 * sl);
+        if (sl != 3) part += ring_term(w1, 2 * sl + 1);  // word 7 is the checksum
+        part += __shfl_xor_sync(0xffffffffu, part, 4);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        const uint64_t pub = shfl64(w0, lane & ~7);
+        const uint64_t chk = shfl64(w1, (lane & ~7) + 3);
+        const bool valid = sj < nb && pub == spos + 1 && part == chk;
+        const bool torn = sj < nb && pub == spos + 1 && part != chk;
+        const unsigned vb = __ballot_sync(0xffffffffu, valid && sl == 0);
+        const unsigned tb = __ballot_sync(0xffffffffu, torn && sl == 0);
+        // consecutive valid segments from segment 0 (bits 0, 8, 16, 24)
+        while (ready < (uint32_t)kMaxBatch && (vb >> (8 * ready)) & 1u) ++ready;
+        if (ready == 0 && tb != 0 && lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
+        if (ready > 0) {
+          const uint64_t t_seen = globaltimer();
+          // No acquire fence: executors read task operands with L2 loads only
+          // (coherence rule, dev_common.cuh), issued after this read returned
+          // (GPUs do not speculate loads past the validation branch).  An
+          // acquire here would run CCTL.IVALL, dropping every warp's L1-resident
+          // stack frames along with stale data (measured: +1.5 us per task).
+          uint64_t ver = shfl64(aux, 1);
+          const uint64_t ye = shfl64(aux, 2);
+          const uint32_t tr = (uint32_t)shfl64(aux, 3);
+          // stage the raw slots of the valid run
+          if ((uint32_t)seg < ready) reinterpret_cast<uint4*>(H->raw[seg])[sl] = v;
+          __syncwarp();
+          for (uint32_t i = 0; i < ready; ++i) {
+            const uint64_t spos = pos + j;
+            const uint64_t* raw = H->raw[i];
+            const int b = next_buffer(F);
+            gpuos_task* task = &H->task[b];
+            SharedCtl* ctl = &H->ctl[b];
+            const bool compact = (raw[6] & 0xff) == kFmtCompact;
+            if (compact) {
+              expand_compact(raw, task, lane);
+            } else {
+              if (lane < 8) reinterpret_cast<uint4*>(task)[lane] = reinterpret_cast<const uint4*>(raw)[lane];
+              __syncwarp();
+              fetch_ext(S, K, spos, task, lane);
+            }
+            __syncwarp();
+            const uint32_t plan = compact ? kPlanDenseSame : plan_task_warp(task, lane);
+            bool shutdown = false;
+            if (lane == 0) {
+              // free the slot for the producer's next lap (queue.hpp:248)
+              st_relaxed_sys((uint64_t*)(K.ring + (spos & K.mask) * kRingSlot), spos + K.cap);
+              const uint64_t claimed = ++H->claimed;
+              if ((claimed & 15) == 0) flush_mirror(K, w, F.mir, claimed, *(volatile uint64_t*)&H->done);
+              ctl->pos = spos;
+              ctl->exit = 0;
+              ctl->t_ticket = t_ticket;
+              ctl->t_seen = t_seen;
+              ctl->yield_every = ye;
+              ctl->trace_on = tr;
+              ctl->plan = plan;
+              if (task->flags & GPUOS_FLAG_SHUTDOWN) {
+                atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)spos);
+                quiesce(K, w);
+                F.my_epoch = kQuiescent;
+                ctl->exit = 1;
+                shutdown = true;
+              } else {
+                if (ver != F.my_epoch) ver = stable_snapshot(S, K, w, ver);
+                F.my_epoch = ver;
+                resolve(S, K, w, H, task->op_id, ver, F.my_epoch, ctl);
+                ctl->version = ver;
+                ctl->t_deq = globaltimer();
+              }
+            }
+            shutdown = __shfl_sync(0xffffffffu, shutdown, 0);
+            __syncwarp();
+            buf_arrive<kBarFull, kFullCount>(b);
+            ++F.k;
+            ++j;
+            if (shutdown) {
+              // the sentinel's buffer carried the first exit marker
+              fetcher_exit(K, w, H, F, lane, true);
+              return;
+            }
+          }
+          spins = 0;
+          expn = 0;
+          continue;
+        }
+      }
+      ++spins;
+      if (lane == 0) {
+        flush_mirror(K, w, F.mir, H->claimed, *(volatile uint64_t*)&H->done);  // idle: counts for wait_all / peek
+        if ((spins & 15) == 0) {
+          const uint64_t cur = ld_relaxed_gpu(&S->version);
+          if (cur != F.my_epoch) F.my_epoch = stable_snapshot(S, K, w, cur);
+          if (spins == K.spin_iterations) atomicAdd((unsigned long long*)&S->stalls, 1ull);
+        }
+      }
+      if (!near) {
+        __nanosleep(64u << expn);
+        if (expn < K.backoff_max_exp) ++expn;
       }
     }
-    if (!near) {
-      __nanosleep(64u << expn);
-      if (expn < K.backoff_max_exp) ++expn;
-    }
   }
-  // Acquire: order this task's data reads after its publication.  The
-  // fence also invalidates this SM's L1 (CCTL.IVALL), so executor loads can
-  // be ordinary L1-allocating loads in a kernel that never relaunches:
-  // buffers rewritten by the host or by other SMs since an earlier task are
-  // re-read from L2.
-  if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  __syncwarp();
-  const uint64_t t_seen = globaltimer();
-  // claim the next ticket now: the atomic's round trip overlaps this task
-  // (not while held: a held worker takes no new ticket, gpuos_dev_hold)
-  if (lane == 0) next = *(volatile uint32_t*)&S->hold ? kNoTicket : atomicAdd((unsigned long long*)&S->claim, 1ull);
-  uint64_t ver = shfl64(aux, 31);
-  const uint64_t ye = shfl64(aux, 30);
-  const uint32_t tr = (uint32_t)shfl64(aux, 29);
-  // stage the descriptor in shared memory
-  if (lane < 24) reinterpret_cast<uint4*>(task)[lane] = v;
-  __syncwarp();
-  if (lane == 0) {
-    // free the slot for the producer's next lap (queue.hpp:248)
-    st_relaxed_sys((uint64_t*)(K.ring + (pos & K.mask) * kTaskBytes), pos + K.cap);
-    const uint64_t claimed = ++H->claimed;
-    if ((claimed & 15) == 0) flush_mirror(K, w, mir, claimed, *(volatile uint64_t*)&H->done);
-    ctl->pos = pos;
-    ctl->exit = 0;
-    ctl->t_ticket = t_ticket;
-    ctl->t_seen = t_seen;
-    ctl->yield_every = ye;
-    ctl->trace_on = tr;
-    if (task->flags & GPUOS_FLAG_SHUTDOWN) {
-      atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)pos);
-      quiesce(K, w);
-      my_epoch = kQuiescent;
-      ctl->exit = 1;
-    } else {
-      if (ver != my_epoch) ver = stable_snapshot(S, K, w, ver);
-      my_epoch = ver;
-      resolve(S, K, w, H, task->op_id, ver, my_epoch, ctl);
-      ctl->version = ver;
-      ctl->t_deq = globaltimer();
-    }
-  }
-  next = shfl64(next, 0);
-  __syncwarp();
-  const uint32_t plan = plan_task_warp(task, lane);
-  if (lane == 0) ctl->plan = plan;
-  __syncwarp();
-  return ctl->exit == 0;
 }
 
 // Completion (runtime.hpp:628-639) by lane 0 of the completer warp.  The
@@ -422,89 +598,43 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   }
   __syncthreads();
   if (warp == 0) {
-    // ---------------- fetcher ----------------
-    WConst K;
-    K.ring = (const char*)S->ring;
-    K.mask = S->mask;
-    K.cap = S->cap;
-    K.host_tail = S->host_tail;
-    K.host_done = S->host_done;
-    K.host_claimed = S->host_claimed;
-    K.host_epoch = S->host_epoch;
-    K.dev_epoch = S->dev_epoch;
-    K.bank[0] = S->bank[0];
-    K.bank[1] = S->bank[1];
-    K.table_slots = S->table_slots;
-    K.spin_iterations = S->spin_iterations;
-    K.backoff_max_exp = S->backoff_max_exp;
-    uint64_t my_epoch = kQuiescent;
-    Mirror mir;
-    mir.flushed_claimed = H->claimed;
-    mir.flushed_done = H->done;
-    uint64_t pos = kNoTicket, t_ticket = 0;
-    uint32_t k = 0;
-    for (;; ++k) {
-      const int b = (int)(k % kBufs);
-      if (k >= kBufs) buf_sync<kBarEmpty, kEmptyCount>(b);
-      if (pos == kNoTicket) {
-        if (lane == 0) {
-          while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
-          pos = atomicAdd((unsigned long long*)&S->claim, 1ull);
-        }
-        pos = shfl64(pos, 0);
-      }
-      t_ticket = globaltimer();  // fetch service starts: ticket in hand, buffer free
-      uint64_t next = 0;
-      const bool more = fetch(S, K, w, H, b, pos, t_ticket, next, my_epoch, mir, lane);
-      buf_arrive<kBarFull, kFullCount>(b);
-      if (!more) break;
-      pos = next;
-    }
-    // drain: wait until the completer released every buffer still in flight
-    // (including the exit marker), then publish the final counts as the
-    // single writer of the host mirrors
-    const uint32_t inflight = k + 1 < (uint32_t)kBufs ? k + 1 : (uint32_t)kBufs;
-    for (uint32_t j = k + 1 - inflight; j <= k; ++j) buf_sync<kBarEmpty, kEmptyCount>((int)(j % kBufs));
-    if (lane == 0) {
-      // a ticket claimed ahead past the sentinel stays unused: the next
-      // generation resumes right after the sentinel (gpuos_dev_start)
-      flush_mirror(K, w, mir, H->claimed, *(volatile uint64_t*)&H->done);
-    }
+    fetcher_main(S, H, w, lane);
     return;
   }
   if (warp == kCompleterWarp) {
-    // ---------------- completer ----------------
+    // ---------------- completer: retires tasks in ticket order ----------------
     uint64_t executed = 0;
+    int exits = 0;
     for (uint32_t k = 0;; ++k) {
       const int b = (int)(k % kBufs);
       buf_sync<kBarDone, kDoneCount>(b);
       const SharedCtl* ctl = &H->ctl[b];
       if (ctl->exit) {
         buf_arrive<kBarEmpty, kEmptyCount>(b);
-        return;
+        if (++exits == kGroups) return;
+        continue;
       }
-      if (lane == 0) {
-        const int code = ctl->code;
-        complete_task(S, w, H, &H->task[b], ctl, code, ctl->t_end, executed);
-      }
+      if (lane == 0) complete_task(S, w, H, &H->task[b], ctl, ctl->code, ctl->t_end, executed);
       __syncwarp();
       buf_arrive<kBarEmpty, kEmptyCount>(b);
     }
   }
-  // ---------------- executors ----------------
+  // ---------------- executor group g: tasks g, g+2, g+4, ... ----------------
+  const int g = (warp - 1) / (kGroupThreads / 32);
   uint32_t dyn;
   asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const int scratch = ((int)dyn - (int)kHeaderBytes) / kGroups & ~127;
   Ctx ctx;
-  ctx.tid = tid - 32;
-  ctx.nthreads = kExecThreads;
+  ctx.tid = tid - 32 - g * kGroupThreads;
+  ctx.nthreads = kGroupThreads;
   ctx.part = 0;
   ctx.nparts = 1;
-  ctx.bar_id = 1;
-  ctx.smem = smem + kHeaderBytes;
-  ctx.smem_bytes = (int)dyn - (int)kHeaderBytes;
+  ctx.bar_id = 1 + g;
+  ctx.smem = smem + kHeaderBytes + g * scratch;
+  ctx.smem_bytes = scratch;
   ctx.aux = 0;
   ctx.flags = 0;
-  for (uint32_t k = 0;; ++k) {
+  for (uint32_t k = (uint32_t)g;; k += kGroups) {
     const int b = (int)(k % kBufs);
     buf_sync<kBarFull, kFullCount>(b);
     gpuos_task* task = &H->task[b];
@@ -521,7 +651,7 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
       const OpFn fn = g_kind_fns[ctl->kind];
       code = fn(task, &ctx);
     }
-    bar_sync<1>(kExecThreads);
+    group_sync(&ctx);
     if (ctx.tid == 0) {
       ctl->code = code;
       ctl->t_fenced = t_wake;
