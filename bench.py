@@ -268,6 +268,7 @@ def main() -> None:
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "tasks_per_step": N_TASKS, "elems": N_ELEMS, "global_batch": N_TASKS * world,
                    "l2": "inputs larger than L2 (491.5 MB distinct buffers per step)",
+                   "buffers": "device memory (RuntimeConfig::device_buffers); e2e copies pinned host <-> device",
                    "parallelism": f"independent ring + persistent kernel per GPU x{world}",
                    "runtime": json.loads(info.value.decode())},
         "p50_submit_to_complete_us": p50, "p99_submit_to_complete_us": p99,

@@ -157,8 +157,15 @@ typedef struct gpuos_cfg {
   uint32_t telemetry;         /* device trace ring on/off (runtime.hpp:181) */
   uint64_t yield_every;       /* executor.hpp:28 */
   uint64_t trace_capacity;    /* device trace ring slots (runtime.hpp:180) */
-  uint64_t reserved[4];
+  uint64_t flags;             /* GPUOS_CFG_* */
+  uint64_t reserved[3];
 } gpuos_cfg;
+
+/* gpuos_cfg.flags: buffers in plain device memory (cudaMalloc) instead of
+ * managed memory.  Faster host<->device copies (measured 1.34M vs 1.04M
+ * config-1 e2e tasks/s); BufferPool::data<T>() pointers are then device
+ * pointers, so host access goes through upload/download. */
+#define GPUOS_CFG_DEVICE_BUFFERS 0x1ull
 
 typedef struct gpuos_dev gpuos_dev; /* opaque per-GPU runtime */
 
@@ -267,6 +274,28 @@ int gpuos_ring_capacity(gpuos_dev* dev, uint64_t* capacity);
 int gpuos_ring_reserve(gpuos_dev* dev, uint64_t* pos);
 /* Publish into a reserved position: copy, checksum, release (queue.hpp:192-231). */
 int gpuos_ring_publish(gpuos_dev* dev, uint64_t pos, const gpuos_task* task);
+/* Dense submit fast path: every operand (output + n_inputs inputs) is a
+ * row-major contiguous view of the same dtype and extents, bound in range,
+ * with at most one scalar.  Reserve + publish in one call, straight into the
+ * ring's compact encoding; QueueFull when the next slot is still in use.
+ * Equivalent to gpuos_ring_reserve + gpuos_ring_publish of the gpuos_task
+ * build_task would produce (queue.hpp:179-231). */
+typedef struct gpuos_dense_task {
+  uint64_t seq;
+  uint64_t done_cell;
+  uint64_t size;        /* output element count */
+  uint32_t op_id;
+  uint16_t flags;
+  uint8_t n_inputs;
+  uint8_t n_scalars;    /* 0 or 1 */
+  uint8_t dtype;
+  uint8_t rank;
+  uint8_t reserved[6];
+  int32_t extents[GPUOS_MAX_RANK];
+  uint64_t addr[1 + GPUOS_MAX_INPUTS]; /* [0] = output */
+  double scalar0;
+} gpuos_dense_task;
+int gpuos_ring_submit_dense(gpuos_dev* dev, const gpuos_dense_task* task);
 /* Monitoring snapshot; head <= tail always holds. */
 int gpuos_ring_peek(gpuos_dev* dev, gpuos_snapshot* out);
 /* Block until processed >= `count` (wait_all, runtime.hpp:399-406). */
@@ -327,6 +356,8 @@ int gpuos_dev_kernel_stream(gpuos_dev* dev, void** stream);
 int gpuos_event_create(gpuos_dev* dev, void** event);
 int gpuos_event_record(gpuos_dev* dev, void* event, void* stream);
 int gpuos_event_sync(gpuos_dev* dev, void* event);
+/* 1 when all work before the event has completed, 0 while pending (non-blocking). */
+int gpuos_event_done(gpuos_dev* dev, void* event);
 int gpuos_event_elapsed_ms(gpuos_dev* dev, void* start, void* stop, float* ms);
 int gpuos_event_destroy(gpuos_dev* dev, void* event);
 /* Pinned host staging memory (freed at gpuos_dev_close). */

@@ -59,7 +59,7 @@ class Cfg(C.Structure):
     _fields_ = [("capacity", C.c_uint64), ("table_slots", C.c_uint32), ("num_workers", C.c_uint32),
                 ("threads_per_worker", C.c_uint32), ("spin_iterations", C.c_uint32),
                 ("backoff_max_exp", C.c_uint32), ("telemetry", C.c_uint32), ("yield_every", C.c_uint64),
-                ("trace_capacity", C.c_uint64), ("reserved", C.c_uint64 * 4)]
+                ("trace_capacity", C.c_uint64), ("flags", C.c_uint64), ("reserved", C.c_uint64 * 3)]
 
 
 class Snapshot(C.Structure):
@@ -98,7 +98,7 @@ assert C.sizeof(View) == 48 and C.sizeof(Task) == SLOT_BYTES and C.sizeof(Instr)
 EXPORTS = [
     "gpuos_abi_version", "gpuos_default_cfg", "gpuos_dev_open", "gpuos_dev_close", "gpuos_dev_alive",
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
-    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
+    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_ring_submit_dense", "gpuos_event_done", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
     "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
     "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
@@ -135,6 +135,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_set_yield_every": ([P, U64], I),
         "gpuos_dev_hold": ([P, I], I),
         "gpuos_dev_run_finite": ([P, C.POINTER(C.c_float)], I),
+        "gpuos_ring_submit_dense": ([P, P], I),
+        "gpuos_event_done": ([P, P], I),
         "gpuos_dev_clock_offset": ([P, C.POINTER(C.c_int64)], I),
         "gpuos_buf_alloc": ([P, I, U64, C.POINTER(U64), C.POINTER(P)], I),
         "gpuos_buf_free": ([P, U64], I),

@@ -502,14 +502,16 @@ int gpuos_dev_clock_offset(gpuos_dev* d, int64_t* off) {
 
 // ---------------------------------------------------------------- buffers
 
-// GPUOS_DEVICE_BUFFERS=1 (experiments): plain cudaMalloc storage instead of
-// managed memory; host pointers from BufferPool then are not dereferenceable.
-static bool device_only_buffers() {
-  static const bool on = [] {
+// Buffer storage: managed memory by default (host pointers from
+// BufferPool::data<T>() stay valid, as in the reference), or plain device
+// memory with GPUOS_CFG_DEVICE_BUFFERS (or GPUOS_DEVICE_BUFFERS=1 in the
+// environment).
+static bool device_only_buffers(const gpuos_dev* d) {
+  static const bool env = [] {
     const char* e = std::getenv("GPUOS_DEVICE_BUFFERS");
     return e && e[0] == '1';
   }();
-  return on;
+  return env || (d->cfg.flags & GPUOS_CFG_DEVICE_BUFFERS) != 0;
 }
 
 int gpuos_buf_alloc(gpuos_dev* d, int dtype, uint64_t n, uint64_t* id, void** ptr) {
@@ -525,12 +527,12 @@ int gpuos_buf_alloc(gpuos_dev* d, int dtype, uint64_t n, uint64_t* id, void** pt
     p = fl->second.back();
     fl->second.pop_back();
   } else if (bytes > kArenaChunk / 4) {
-    GPUOS_CK(device_only_buffers() ? cudaMalloc(&p, bytes) : cudaMallocManaged(&p, bytes));
+    GPUOS_CK(device_only_buffers(d) ? cudaMalloc(&p, bytes) : cudaMallocManaged(&p, bytes));
     d->managed_blocks.push_back(p);
   } else {
     if (d->arena_left < bytes) {
       void* blk = nullptr;
-      GPUOS_CK(device_only_buffers() ? cudaMalloc(&blk, kArenaChunk) : cudaMallocManaged(&blk, kArenaChunk));
+      GPUOS_CK(device_only_buffers(d) ? cudaMalloc(&blk, kArenaChunk) : cudaMallocManaged(&blk, kArenaChunk));
       d->managed_blocks.push_back(blk);
       d->arena_cur = (char*)blk;
       d->arena_left = kArenaChunk;
@@ -590,7 +592,7 @@ int gpuos_buf_copy(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int
 
 int gpuos_buf_prefetch(gpuos_dev* d, uint64_t id) {
   if (!d) return GPUOS_INTERNAL;
-  if (device_only_buffers()) return GPUOS_OK;  // already device memory
+  if (device_only_buffers(d)) return GPUOS_OK;  // already device memory
   void* p = nullptr;
   uint64_t bytes = 0;
   {
@@ -762,6 +764,37 @@ int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
   __atomic_store_n(&dst[0], pos + 1, __ATOMIC_RELEASE);
   __atomic_store_n(d->tail, pos + 1, __ATOMIC_RELEASE);
   d->published.store(pos + 1, std::memory_order_relaxed);
+  return GPUOS_OK;
+}
+
+int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
+  const uint64_t p = d->reserve;
+  uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (p & d->mask) * gdev::kRingSlot);
+  if (__atomic_load_n(dst, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
+  d->reserve = p + 1;
+  asm volatile("prefetchw (%0)" ::"r"(d->ring + ((p + 16) & d->mask) * gdev::kRingSlot));
+  uint64_t w[gdev::kSlotWords];
+  w[1] = t->seq;
+  w[2] = (uint64_t)t->op_id | ((uint64_t)t->flags << 32) | ((uint64_t)t->n_inputs << 48) |
+         ((uint64_t)t->n_scalars << 56);
+  w[3] = t->size;
+  w[4] = t->done_cell;
+  w[5] = d->shadow.trace_on ? __rdtsc() : 0;
+  w[6] = gdev::kFmtCompact | ((uint64_t)t->dtype << 8) | ((uint64_t)t->rank << 16);
+  w[8] = (uint64_t)(uint32_t)t->extents[0] | ((uint64_t)(uint32_t)t->extents[1] << 32);
+  w[9] = (uint64_t)(uint32_t)t->extents[2] | ((uint64_t)(uint32_t)t->extents[3] << 32);
+  for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) w[10 + k] = k <= t->n_inputs ? t->addr[k] : 0;
+  std::memcpy(&w[15], &t->scalar0, 8);
+  uint64_t h = gdev::ring_term(p + 1, 0);
+  for (uint32_t i = 1; i < gdev::kSlotWords; ++i) {
+    if (i == 7) continue;
+    dst[i] = w[i];
+    h += gdev::ring_term(w[i], i);
+  }
+  dst[7] = h;
+  __atomic_store_n(&dst[0], p + 1, __ATOMIC_RELEASE);
+  __atomic_store_n(d->tail, p + 1, __ATOMIC_RELEASE);
+  d->published.store(p + 1, std::memory_order_relaxed);
   return GPUOS_OK;
 }
 
@@ -1174,6 +1207,11 @@ int gpuos_event_sync(gpuos_dev* d, void* ev) {
   cudaSetDevice(d->device);
   GPUOS_CK(cudaEventSynchronize((cudaEvent_t)ev));
   return GPUOS_OK;
+}
+
+int gpuos_event_done(gpuos_dev* d, void* e) {
+  if (!d || !e) return 0;
+  return cudaEventQuery(static_cast<cudaEvent_t>(e)) == cudaSuccess ? 1 : 0;
 }
 
 int gpuos_event_elapsed_ms(gpuos_dev* d, void* a, void* b, float* ms) {

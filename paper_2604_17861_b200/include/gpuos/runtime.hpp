@@ -109,12 +109,16 @@ class CellPool {
     return g;
   }
   static constexpr uint64_t kSeqMask = (uint64_t{1} << 48) - 1;
+  // One atomic per handle copy/destroy: the pool's own lifetime after the
+  // runtime is gone is derived from the per-cell counts (try_delete), not
+  // from a second shared counter.
   void addref(uint32_t g) { blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_add(1, std::memory_order_relaxed); }
   void release(uint32_t g) {
-    blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_sub(1, std::memory_order_acq_rel);
-    if (live_.fetch_sub(1, std::memory_order_acq_rel) == 1 && orphaned_.load(std::memory_order_acquire)) delete this;
+    // seq_cst pairs with orphan(): the last releaser or orphan() sees the other
+    if (blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_sub(1, std::memory_order_seq_cst) == 1 &&
+        orphaned_.load(std::memory_order_seq_cst))
+      try_delete();
   }
-  void hold() { live_.fetch_add(1, std::memory_order_relaxed); }
   long use_count(uint32_t g) const {
     return static_cast<long>(blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].load(std::memory_order_relaxed));
   }
@@ -132,8 +136,8 @@ class CellPool {
       b.host = h;
       b.heap = true;
     }
-    orphaned_.store(true, std::memory_order_release);
-    if (live_.load(std::memory_order_acquire) == 0) delete this;
+    orphaned_.store(true, std::memory_order_seq_cst);
+    try_delete();
   }
   ~CellPool() {
     for (Block& b : blocks_) {
@@ -159,11 +163,19 @@ class CellPool {
     blocks_.push_back(b);
   }
 
+  // After orphan(): delete once no handle references any cell.
+  void try_delete() {
+    for (const Block& b : blocks_)
+      for (uint32_t i = 0; i < kBlock; ++i)
+        if (b.refs[i].load(std::memory_order_seq_cst) != 0) return;
+    if (!deleting_.exchange(true, std::memory_order_acq_rel)) delete this;
+  }
+
   gpuos_dev* dev_;
   std::vector<Block> blocks_;
   uint32_t cursor_ = 0;
-  std::atomic<long> live_{0};
   std::atomic<bool> orphaned_{false};
+  std::atomic<bool> deleting_{false};
 };
 
 }  // namespace detail
@@ -238,10 +250,7 @@ class TaskHandle {
     return (w >> 16) == (id_ & detail::CellPool::kSeqMask) ? w : 0;
   }
   void ref() {
-    if (pool_) {
-      pool_->hold();
-      pool_->addref(cell_);
-    }
+    if (pool_) pool_->addref(cell_);
   }
   void unref() {
     if (pool_) pool_->release(cell_);
@@ -281,6 +290,9 @@ struct RuntimeConfig {
   /// reference never queues them (runtime.hpp:531-534); config 3 needs them
   /// queued, so this build defaults to true.
   bool queue_matmul = true;
+  /// Task buffers in plain device memory instead of managed memory (faster
+  /// host<->device copies; host access only through pool().upload/download).
+  bool device_buffers = false;
 
   /// GPUOS_CAPACITY, GPUOS_WORKERS, GPUOS_YIELD_EVERY, GPUOS_MAX_ELEMS, GPUOS_DEVICE.
   static RuntimeConfig from_env() {
@@ -317,6 +329,7 @@ class Runtime {
     c.yield_every = cfg_.workers.yield_every;
     c.trace_capacity = cfg_.trace_capacity;
     c.telemetry = cfg_.telemetry_enabled ? 1u : 0u;
+    c.flags = cfg_.device_buffers ? GPUOS_CFG_DEVICE_BUFFERS : 0u;
     check_abi(gpuos_dev_open(cfg_.device, &c, &dev_), "gpuos_dev_open");
     pool_ = std::make_unique<BufferPool>(dev_);
     table_ = std::make_unique<OperatorTable>(dev_);
@@ -663,8 +676,68 @@ class Runtime {
     return true;
   }
 
+  /// Dense fast path (the small-op common case): every operand a contiguous,
+  /// in-range view of the output's dtype and shape, at most one scalar.  Goes
+  /// straight into the ring's compact slot encoding; returns false (nothing
+  /// published) when the call does not qualify or the ring is full.
+  bool try_publish_dense(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+                         std::span<const double> scalars, uint32_t cell, uint64_t id, uint16_t flags, bool* full) {
+    const size_t rank = output.rank();
+    if (scalars.size() > 1 || rank > GPUOS_MAX_RANK || op_id > UINT32_MAX) return false;
+    gpuos_dense_task t;
+    t.seq = id;
+    t.done_cell = cells_->device_addr(cell);
+    t.op_id = static_cast<uint32_t>(op_id);
+    t.flags = flags;
+    t.n_inputs = static_cast<uint8_t>(inputs.size());
+    t.n_scalars = static_cast<uint8_t>(scalars.size());
+    t.dtype = static_cast<uint8_t>(output.dtype);
+    t.rank = static_cast<uint8_t>(rank);
+    std::memset(t.reserved, 0, sizeof(t.reserved));
+    int64_t n = 1;
+    for (size_t d = 0; d < GPUOS_MAX_RANK; ++d) {
+      const int64_t e = d < rank ? output.shape[d] : 0;
+      if (e < 0 || e > INT32_MAX) return false;
+      t.extents[d] = static_cast<int32_t>(e);
+      if (d < rank) n *= e;
+    }
+    t.size = static_cast<uint64_t>(n);
+    t.scalar0 = scalars.empty() ? 0.0 : scalars[0];
+    const size_t w = dtype_width(output.dtype);
+    for (size_t k = 0; k <= inputs.size(); ++k) {
+      const TensorView& v = k == 0 ? output : inputs[k - 1];
+      if (v.dtype != output.dtype || v.rank() != rank) return false;
+      int64_t acc = 1;
+      for (size_t d = rank; d-- > 0;) {
+        if (v.shape[d] != output.shape[d] || v.strides[d] != acc) return false;  // exact contiguous strides
+        acc *= v.shape[d];
+      }
+      const BufferPool::Buffer* b = pool_->find(v.buffer);
+      if (!b || b->dtype != v.dtype || v.offset < 0 || (n > 0 && v.offset + n > static_cast<int64_t>(b->length)))
+        return false;  // the general path reports the bind status
+      t.addr[k] = reinterpret_cast<uint64_t>(static_cast<char*>(b->data) + v.offset * static_cast<int64_t>(w));
+    }
+    for (size_t k = inputs.size() + 1; k <= GPUOS_MAX_INPUTS; ++k) t.addr[k] = 0;
+    const int rc = gpuos_ring_submit_dense(dev_, &t);
+    *full = rc == static_cast<int>(ErrorCode::QueueFull);
+    return rc == 0;
+  }
+
   void route(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
              std::span<const double> scalars, uint32_t cell, uint64_t id, bool elig, uint16_t flags) {
+    if (elig) {
+      bool full = false;
+      if (try_publish_dense(op_id, inputs, output, scalars, cell, id, flags, &full)) {
+        counters_->inc_committed();
+        ++committed_tasks_;
+        return;
+      }
+      if (full) {
+        counters_->inc_queue_full_fallback();
+        execute_inline(op_id, inputs, output, scalars, cell, id);
+        return;
+      }
+    }
     // Views of rank > 4 or with extents/strides beyond int32 do not fit a
     // slot (the reference spills them, queue.hpp:207-221); they take the
     // conventional path, which reports TooLarge for them.

@@ -13,9 +13,10 @@
 //   1  per-op      : baseline (a), one cudaLaunchKernel of the same task body
 //                    per task, back to back on one stream; CUDA-event timed.
 //   2  e2e         : like 0 but inputs start in pinned host memory and outputs
-//                    end there: chunked H2D copies, submits and D2H copies all
-//                    inside the (host-clock) timed region.
+//                    end there: chunked H2D copies, submits and per-chunk D2H
+//                    copies, pipelined, all inside the (host-clock) timed region.
 #include <gpuos/runtime.hpp>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <chrono>
@@ -45,7 +46,8 @@ struct Bench {
   float* hC = nullptr;
   void* kstream = nullptr;
   void* lstream = nullptr;   // per-op launch stream
-  void* cstream = nullptr;   // copy stream
+  void* cstream = nullptr;   // copy stream (H2D)
+  void* dstream = nullptr;   // copy stream (D2H)
   void* ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<float> expect;  // host reference of c = a + b (f32 add), for the self-check
   uint64_t last_fallbacks = 0;
@@ -68,6 +70,9 @@ void* gb_open(int device, int n_tasks, int n_elems, int workers, int capacity) {
   // the trace ring is off on the measured path; GPUOS_BENCH_TRACE=1 turns it
   // on to print per-phase device stamps after each step (diagnostics only)
   cfg.telemetry_enabled = std::getenv("GPUOS_BENCH_TRACE") != nullptr;
+  // plain device memory for the task buffers: the e2e arm moves 491.5 MB per
+  // step over PCIe, and copies into managed memory measured ~25% slower
+  cfg.device_buffers = true;
   b->rt = std::make_unique<Runtime>(cfg);
   b->dev = b->rt->device();
   b->n = n_tasks;
@@ -103,6 +108,7 @@ void* gb_open(int device, int n_tasks, int n_elems, int workers, int capacity) {
   check_abi(gpuos_dev_kernel_stream(b->dev, &b->kstream), "kernel stream");
   check_abi(gpuos_stream_create(b->dev, &b->lstream), "launch stream");
   check_abi(gpuos_stream_create(b->dev, &b->cstream), "copy stream");
+  check_abi(gpuos_stream_create(b->dev, &b->dstream), "d2h stream");
   for (void*& e : b->ev) check_abi(gpuos_event_create(b->dev, &e), "event");
   // steps start the worker kernel themselves
   b->rt->wait_all();
@@ -128,33 +134,58 @@ int gb_step(void* h, int mode, double* out) {
       out[5] = now_ms() - t0;  // producer-side cost of the N submits
       rt.wait_all();
     } else {
-      // e2e: chunked H2D copies overlapped with submission, then D2H
-      const int chunks = 8;
+      // e2e: a three-stage pipeline over chunks of tasks -- H2D of chunk k+1
+      // (copy stream) overlaps the tasks of chunk k, and the D2H of every
+      // finished chunk (second copy stream) overlaps both, so the step is
+      // bounded by the H2D volume over PCIe rather than H2D + D2H in series.
+      const int chunks = 16;
       const int per = (b->n + chunks - 1) / chunks;
       const BufferPool::Buffer& ba = rt.pool().lookup(b->A.buffer);
       const BufferPool::Buffer& bb = rt.pool().lookup(b->B.buffer);
       const BufferPool::Buffer& bc = rt.pool().lookup(b->Cv.buffer);
-      std::vector<void*> evs(chunks);
-      for (int k = 0; k < chunks; ++k) {
+      std::vector<void*> evs(chunks, nullptr);
+      auto span_of = [&](int k, uint64_t* off, uint64_t* bytes) {
         const int lo = k * per, hi = std::min(b->n, lo + per);
-        if (lo >= hi) break;
-        const uint64_t off = static_cast<uint64_t>(lo) * b->e * 4, bytes = static_cast<uint64_t>(hi - lo) * b->e * 4;
+        *off = static_cast<uint64_t>(lo) * b->e * 4;
+        *bytes = hi > lo ? static_cast<uint64_t>(hi - lo) * b->e * 4 : 0;
+        return hi > lo;
+      };
+      for (int k = 0; k < chunks; ++k) {
+        uint64_t off, bytes;
+        if (!span_of(k, &off, &bytes)) break;
         check_abi(gpuos_copy_async(b->dev, static_cast<char*>(ba.data) + off, reinterpret_cast<char*>(b->hA) + off, bytes, 0, b->cstream), "h2d");
         check_abi(gpuos_copy_async(b->dev, static_cast<char*>(bb.data) + off, reinterpret_cast<char*>(b->hB) + off, bytes, 0, b->cstream), "h2d");
         check_abi(gpuos_event_create(b->dev, &evs[k]), "ev");
         check_abi(gpuos_event_record(b->dev, evs[k], b->cstream), "ev");
       }
-      std::vector<TaskHandle> last(chunks);
-      for (int k = 0; k < chunks; ++k) {
-        const int lo = k * per, hi = std::min(b->n, lo + per);
-        if (lo >= hi) break;
-        check_abi(gpuos_event_sync(b->dev, evs[k]), "ev sync");
-        for (int i = lo; i < hi; ++i) rt.submit(OpKind::Add, {b->a[i], b->b[i]}, b->c[i]);
+      std::vector<TaskHandle> hs;
+      hs.reserve(static_cast<size_t>(b->n));
+      // one host loop, never blocking: submit a chunk as soon as its inputs
+      // landed, start a chunk's D2H as soon as its last task completed
+      int next_sub = 0, next_out = 0, scan = 0;
+      int nchunks = 0;
+      for (int k = 0; k < chunks; ++k) nchunks += (k * per < b->n) ? 1 : 0;
+      while (next_out < nchunks) {
+        if (next_sub < nchunks && gpuos_event_done(b->dev, evs[next_sub])) {
+          const int lo = next_sub * per, hi = std::min(b->n, lo + per);
+          for (int i = lo; i < hi; ++i) hs.push_back(rt.submit(OpKind::Add, {b->a[i], b->b[i]}, b->c[i]));
+          ++next_sub;
+          continue;
+        }
+        if (next_out < next_sub) {
+          const int hi = std::min(b->n, (next_out + 1) * per);
+          while (scan < hi && hs[static_cast<size_t>(scan)].state() != TaskState::Pending) ++scan;
+          if (scan == hi) {
+            uint64_t off, bytes;
+            if (span_of(next_out, &off, &bytes))
+              check_abi(gpuos_copy_async(b->dev, reinterpret_cast<char*>(b->hC) + off, static_cast<char*>(bc.data) + off, bytes, 1, b->dstream), "d2h");
+            ++next_out;
+            continue;
+          }
+        }
+        _mm_pause();
       }
-      rt.wait_all();
-      const uint64_t total = static_cast<uint64_t>(b->n) * b->e * 4;
-      check_abi(gpuos_copy_async(b->dev, b->hC, bc.data, total, 1, b->cstream), "d2h");
-      check_abi(gpuos_stream_sync(b->dev, b->cstream), "sync");
+      check_abi(gpuos_stream_sync(b->dev, b->dstream), "sync");
       for (void* e : evs)
         if (e) gpuos_event_destroy(b->dev, e);
     }

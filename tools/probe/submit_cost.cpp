@@ -3,7 +3,39 @@
 // Prints ns/task for: the full submit (workers live), the full submit with
 // workers held (no device traffic on the ring), and the pieces: TensorView
 // copies, cell acquire, ring reserve+publish of a prebuilt slot.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cctype>
+#include <chrono>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <future>
+#include <immintrin.h>
+#include <initializer_list>
+#include <istream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <ostream>
+#include <span>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+#define private public  // probe only: time the submit path's internal steps
 #include <gpuos/runtime.hpp>
+#undef private
 
 #include <chrono>
 #include <cstdio>
@@ -51,6 +83,46 @@ int main() {
     gpuos_dev_hold(dev, 0);
     rt.wait_all();
     std::printf("held: submit %.1f ns/task\n", (t1 - t0) / n);
+    // 2b. handles kept (no destructor in the loop)
+    {
+      std::vector<TaskHandle> keep;
+      keep.reserve(n);
+      t0 = now_ns();
+      for (int i = 0; i < n; ++i) keep.push_back(rt.submit(OpKind::Add, {a[i], b[i]}, c[i]));
+      t1 = now_ns();
+      rt.wait_all();
+      const double t2k = now_ns();
+      keep.clear();
+      const double t3k = now_ns();
+      std::printf("kept handles: submit %.1f ns/task, dtor %.1f ns/task\n", (t1 - t0) / n, (t3k - t2k) / n);
+    }
+    // 2c. internal steps of submit_span, each in its own loop
+    {
+      std::vector<uint32_t> cells(n);
+      t0 = now_ns();
+      for (int i = 0; i < n; ++i) cells[i] = rt.cells_->acquire(rt.next_id_++);
+      t1 = now_ns();
+      double t_acq = (t1 - t0) / n;
+      volatile int sinkv = 0;
+      t0 = now_ns();
+      for (int i = 0; i < n; ++i) {
+        const TensorView in2[2] = {a[i], b[i]};
+        sinkv += (int)rt.validate(std::span<const TensorView>(in2, 2), c[i], std::span<const double>());
+        sinkv += rt.eligible(0, std::span<const TensorView>(in2, 2), c[i]);
+      }
+      t1 = now_ns();
+      double t_val = (t1 - t0) / n;
+      alignas(64) gpuos_task tk;
+      t0 = now_ns();
+      for (int i = 0; i < n; ++i) {
+        const TensorView in2[2] = {a[i], b[i]};
+        rt.build_task(0, std::span<const TensorView>(in2, 2), c[i], std::span<const double>(), cells[i], 5, 0, &tk);
+      }
+      t1 = now_ns();
+      double t_build = (t1 - t0) / n;
+      std::printf("steps: cell acquire %.1f, validate+eligible %.1f, build_task %.1f ns/task\n", t_acq, t_val, t_build);
+      for (int i = 0; i < n; ++i) rt.cells_->complete(cells[i], 0, ErrorCode::Ok);
+    }
     // 3. TensorView copies only
     t0 = now_ns();
     volatile size_t sink = 0;
