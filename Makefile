@@ -35,8 +35,8 @@ $(LIBDIR)/libgpuos_cuda.so: $(OBJ)/worker.o $(OBJ)/capi.o
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
-$(LIBDIR)/libgpuos_bench.so: tools/bench/gpuos_bench.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
-	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN'
+$(LIBDIR)/libgpuos_bench.so: tools/bench/gpuos_bench.cpp tools/bench/gpuos_bench_configs.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	$(CXX) $(CXXFLAGS) -shared -o $@ tools/bench/gpuos_bench.cpp tools/bench/gpuos_bench_configs.cpp -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN'
 
 build/cpp/test_runtime: tests/cpp/test_runtime.cpp tests/cpp/check.hpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	@mkdir -p build/cpp

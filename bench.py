@@ -166,6 +166,40 @@ def run_reference(args) -> None:
     print(json.dumps(line))
 
 
+def run_configs(lib, local: int) -> dict:
+    """BASELINE.json configs 2-4 on this GPU (tools/bench/gpuos_bench_configs.cpp)."""
+    peaks = load_peaks()
+    lib.gb_config2.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_config3.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_config4.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
+    out = (C.c_double * 16)()
+    res = {}
+    lib.gb_config2(local, 20_000, 3, out)
+    res["config2_mixed"] = {
+        "workload": "mixed {add,mul,relu,reduce_sum} x {f32,f16,bf16,i32}, numel log-uniform 64..65536, "
+                    "contiguous/strided/broadcast layouts, seed 42; 20,000 tasks per step, distinct outputs",
+        "tasks_per_s": out[0], "alg_GBps": out[1], "roofline_frac": out[1] / peaks["hbm_gbs"],
+        "mean_bytes_per_task": out[3], "failed_tasks": int(out[4]), "host_submit_ns_per_task": out[5]}
+    for name, dt in (("config3_attention_f32", 0), ("config3_attention_bf16", 4)):
+        lib.gb_config3(local, dt, 20, out)
+        res[name] = {
+            "workload": "32 heads x seq 128 x head_dim 64: Q*scale, Q.K^T (transposed view), softmax, P.V as "
+                        "128 individual tasks per step, host waits between the 4 phases",
+            "step_us": out[0], "tasks_per_s": out[1], "gflops": out[2], "failed_tasks": int(out[3]),
+            "max_rel_err_head0": out[4]}
+    lib.gb_config4(local, 1_000_000, out)
+    res["config4_hot_swap"] = {
+        "workload": "1,000,000 fp32 4096-element tasks alternating builtin add and injected scale_add(1.5,-0.25); "
+                    "scale_add re-injected as (-2,3) at task 500,000 with the 4096-slot ring full (streaming "
+                    "reading of '1M in flight')",
+        "tasks_per_s": out[0], "inject_call_ms": out[1],
+        "swap_phases_us": {"upload": out[2], "epoch_wait": out[3], "bank_write": out[4], "flip": out[5]},
+        "window_rows_checked": int(out[6]), "rows_not_one_variant": int(out[7]),
+        "old_rows_past_window": int(out[8]), "failed_tasks": int(out[9]), "canary_hits": int(out[10]),
+        "old_rows": int(out[11]), "new_rows": int(out[12])}
+    return res
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -176,6 +210,7 @@ def main() -> None:
     ap.add_argument("--capacity", type=int, default=4096)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2-4 lines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -240,6 +275,7 @@ def main() -> None:
     info = C.create_string_buffer(512)
     lib.gb_info(h, info, 512)
     lib.gb_close(h)
+    configs = None if (args.no_configs or world > 1) else run_configs(lib, local)
 
     if rank != 0:
         dist_barrier(dist)
@@ -285,6 +321,7 @@ def main() -> None:
         "gpu_launches": args.steps,
         "parity": {"mismatches": bad.value, "checked": checked.value, "e2e_mismatches": e_bad.value},
         "queue_full_fallbacks": fallbacks,
+        "configs": configs,
         "clocks": clk,
     }
     print(json.dumps(line))
