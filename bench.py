@@ -186,7 +186,8 @@ def run_configs(lib, local: int) -> dict:
             "workload": "32 heads x seq 128 x head_dim 64: Q*scale, Q.K^T (transposed view), softmax, P.V as "
                         "128 individual tasks per step, host waits between the 4 phases",
             "step_us": out[0], "tasks_per_s": out[1], "gflops": out[2], "failed_tasks": int(out[3]),
-            "max_rel_err_head0": out[4]}
+            "max_rel_err_head0": out[4],
+            "phase_us": {"scale": out[5], "qk_t": out[6], "softmax": out[7], "pv": out[8]}}
     lib.gb_config4(local, 1_000_000, out)
     res["config4_hot_swap"] = {
         "workload": "1,000,000 fp32 4096-element tasks alternating builtin add and injected scale_add(1.5,-0.25); "

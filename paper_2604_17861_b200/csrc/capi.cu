@@ -261,16 +261,18 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
 
   d->threads = cfg.threads_per_worker;
   d->smem = gdev::worker_smem_bytes();
-  // default: one worker CTA per SM.  A second CTA per SM
-  // would fit (288 threads, <=112 registers, 96 KB shared), but then the
-  // conventional path's standalone kernels and the runtime's memsets could
-  // not be scheduled next to a resident generation; num_workers can still
-  // ask for up to worker_occupancy() per SM.
+  // One worker CTA per SM: a second one would leave no room
+  // (registers, shared memory, TMEM) for the conventional path's standalone
+  // kernels and the runtime's memsets next to a resident generation.
   int per_sm = 0;
   GPUOS_CK(gdev::worker_occupancy(&per_sm));
   if (per_sm < 1) per_sm = 1;
+  // At most one worker CTA per SM: each holds 256 of the SM's 512 TMEM
+  // columns for its tensor-core GEMMs, and a standalone matmul kernel of the
+  // conventional path must still be able to allocate the rest.
+  (void)per_sm;
   d->workers = cfg.num_workers ? cfg.num_workers : d->sms;
-  if (d->workers > d->sms * (uint32_t)per_sm) d->workers = d->sms * (uint32_t)per_sm;
+  if (d->workers > d->sms) d->workers = d->sms;
   if (d->workers > gdev::kMaxWorkers) d->workers = gdev::kMaxWorkers;
 
   // ring capacity: power of two, min 2 (queue.hpp:164-165)

@@ -27,7 +27,11 @@ struct Ctx {
   char* smem;       // shared-memory scratch (no static __shared__ in bodies)
   uint64_t aux;     // table-entry payload (program pointer for KIND_PROGRAM)
   uint32_t flags;   // task flags (GPUOS_FLAG_UNCAPPED, ...)
+  uint32_t tmem;    // this group's 128 TMEM columns (kNoTmem = none)
+  uint64_t* mbar;   // this group's MMA-completion mbarrier (shared memory)
+  uint32_t* mma_phase;  // its current phase bit (shared memory)
 };
+constexpr uint32_t kNoTmem = 0xffffffffu;
 
 typedef int (*OpFn)(const gpuos_task* t, const Ctx* c);
 

@@ -5,11 +5,12 @@
 // Accumulation order matches the reference exactly (ascending k, one rounding
 // per product and per add).  For f32/f16/bf16 operands every product is exact
 // in fp64, so a DFMA equals the reference's separate multiply and add and is
-// used; f64/i32 operands use __dmul_rn + __dadd_rn.  The bf16/f16 tensor-core
-// (tcgen05) GEMM lives in ops_umma.cuh.
+// used; f64/i32 operands use __dmul_rn + __dadd_rn.  bf16/f16 matmuls run on
+// the tensor cores (tcgen05, ops_umma.cuh) when the executing group has TMEM.
 #pragma once
 
 #include "dev_common.cuh"
+#include "ops_umma.cuh"
 
 namespace gdev {
 
@@ -39,6 +40,10 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
   int bc;
   if ((bc = bind_code(a)) || (bc = bind_code(b)) || (bc = bind_code(out))) return bc;
   const int dt = out.dtype;
+  // 16-bit floats: tensor cores (tcgen05, ops_umma.cuh) when the group holds TMEM
+  if ((dt == GPUOS_BF16 || dt == GPUOS_F16) && c->tmem != kNoTmem && c->smem_bytes >= 2 * (int)kUmmaTileBytes &&
+      m > 0 && n > 0 && k > 0)
+    return matmul_umma(a, b, out, m, k, n, c);
   const bool exact = exact_products(dt);
   const char* ap = (const char*)a.addr;
   const char* bp = (const char*)b.addr;

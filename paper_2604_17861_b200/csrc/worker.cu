@@ -92,6 +92,8 @@ constexpr int kBufs = 4;
 constexpr int kBarFull = 3, kBarDone = 7, kBarEmpty = 11;
 constexpr int kFullCount = 32 + kGroupThreads, kDoneCount = kGroupThreads + 32, kEmptyCount = 64;
 constexpr int kMaxBatch = 4;  // tickets claimed per atomic / slots per warp-wide read
+constexpr uint32_t kTmemCols = 256;  // 128 per executor group; the rest stays free for standalone kernels
+constexpr int kBarExecExit = 15;  // both executor groups, before TMEM is released
 // Per-CTA cache of resolved table entries, tagged with the version they were
 // resolved under: an entry of version v is immutable while v is current
 // (the host rewrites a bank only after every epoch moved past it), so a tag
@@ -114,6 +116,10 @@ struct WorkerHeader {
   uint64_t raw[kMaxBatch][kSlotWords];  // slots as read, before expansion
   uint64_t done;                        // tasks completed by this CTA (all generations)
   uint64_t claimed;                     // tickets claimed by this CTA (all generations)
+  uint64_t mbar[kGroups];               // per-group tensor-core completion barriers
+  uint32_t mma_phase[kGroups];
+  uint32_t tmem_base;                   // kTmemCols columns, kTmemCols/kGroups per group
+  uint32_t pad_;
   CachedEntry cache[kEntryCache];
 };
 static_assert(sizeof(WorkerHeader) <= kHeaderBytes, "worker header overflows");
@@ -596,7 +602,17 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
     H->cache[i].version = kQuiescent;
     H->cache[i].op_id = 0xffffffffu;
   }
+  if (tid == 0) {
+    for (int g = 0; g < kGroups; ++g) {
+      mbar_init(&H->mbar[g], 1);
+      H->mma_phase[g] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&H->tmem_base, kTmemCols);  // owned (and released) by warp 1
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
   if (warp == 0) {
     fetcher_main(S, H, w, lane);
     return;
@@ -634,6 +650,9 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   ctx.smem_bytes = scratch;
   ctx.aux = 0;
   ctx.flags = 0;
+  ctx.tmem = H->tmem_base + (uint32_t)(g * (kTmemCols / kGroups));
+  ctx.mbar = &H->mbar[g];
+  ctx.mma_phase = &H->mma_phase[g];
   for (uint32_t k = (uint32_t)g;; k += kGroups) {
     const int b = (int)(k % kBufs);
     buf_sync<kBarFull, kFullCount>(b);
@@ -641,6 +660,11 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
     SharedCtl* ctl = &H->ctl[b];
     if (ctl->exit) {
       buf_arrive<kBarDone, kDoneCount>(b);
+      // both groups are past their last tensor-core use: release TMEM
+      tc_fence_before();
+      bar_sync<kBarExecExit>(kGroups * kGroupThreads);
+      tc_fence_after();
+      if (warp == 1) tmem_dealloc(H->tmem_base, kTmemCols);
       return;
     }
     const uint64_t t_wake = globaltimer();
@@ -699,6 +723,19 @@ __global__ void __launch_bounds__(256, 3) gpuos_task_kernel(const gpuos_task tas
   for (int i = threadIdx.x; i < (int)(sizeof(gpuos_task) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(t)[i] = src[i];
   uint32_t* plan_s = reinterpret_cast<uint32_t*>(smem + kTaskBytes);
+  uint32_t* tmem_s = plan_s + 1;
+  uint32_t* phase_s = plan_s + 2;
+  uint64_t* mbar_s = reinterpret_cast<uint64_t*>(smem + kTaskBytes + 16);
+  constexpr bool kTensor = KIND == GPUOS_OP_MATMUL_SMALL;
+  if (kTensor) {
+    if (threadIdx.x == 0) {
+      mbar_init(mbar_s, 1);
+      *phase_s = 0;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) tmem_alloc(tmem_s, 128);
+    tc_fence_before();
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
     const uint32_t plan = plan_task_warp(t, threadIdx.x);
@@ -717,7 +754,17 @@ __global__ void __launch_bounds__(256, 3) gpuos_task_kernel(const gpuos_task tas
   ctx.smem_bytes = (int)dyn - (int)(kTaskBytes + kCtlBytes);
   ctx.aux = aux;
   ctx.flags = t->flags | *plan_s;
+  if (kTensor) tc_fence_after();
+  ctx.tmem = kTensor ? *tmem_s : kNoTmem;
+  ctx.mbar = mbar_s;
+  ctx.mma_phase = phase_s;
   const int code = body<KIND>(t, &ctx);
+  if (kTensor) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x < 32) tmem_dealloc(*tmem_s, 128);
+  }
   __syncthreads();
   if (threadIdx.x == 0 && t->done_cell) {
     bool last = true;

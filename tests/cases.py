@@ -173,7 +173,8 @@ def linalg_cases(seed=13, dtypes=ALL_DTYPES) -> List[Case]:
         for (m, k, n) in ((128, 64, 128), (128, 128, 64), (37, 19, 53), (256, 256, 256), (1, 70, 3)):
             a = layout(rng, [m, k], dt, "contig", "mul" if dt == I32 else "add", lo, hi)
             b = layout(rng, [k, n], dt, "transposed" if n == k else "contig", "mul" if dt == I32 else "add", lo, hi)
-            rule = "exact"
+            # f16/bf16 run on the tensor cores: fp32 accumulation (bound in parity.compare)
+            rule = "gemm32" if dt in (F16, BF16) else "exact"
             cases.append(Case(f"matmul-{dt}-{m}x{k}x{n}", "matmul_small", dt, [a, b], out_operand([m, n], dt), [], rule))
         a = layout(rng, [16, 257], dt, "contig", "mul", lo, hi)
         b = layout(rng, [257, 8], dt, "contig", "mul", lo, hi)

@@ -68,6 +68,17 @@ def device_run(dev, case: Case, inline: bool = False):
     return rc, outs
 
 
+def logical(op: Operand) -> np.ndarray:
+    """The view's logical values (after narrowing to its dtype), shape op.shape."""
+    vals = ol.decode(storage(op), op.dtype)
+    idx = np.full(op.shape, op.offset, dtype=np.int64) if op.shape else np.array(op.offset)
+    for d, (e, s) in enumerate(zip(op.shape, op.strides)):
+        sh = [1] * len(op.shape)
+        sh[d] = e
+        idx = idx + (np.arange(e, dtype=np.int64) * s).reshape(sh)
+    return vals[idx]
+
+
 def _ulp_dist(a: np.ndarray, b: np.ndarray, dtype: int) -> np.ndarray:
     """|ordered-integer distance| between encodings (NaN handled by callers)."""
     if dtype == F32:
@@ -111,6 +122,23 @@ def compare(case: Case, got: np.ndarray, want: np.ndarray, dtype: int) -> Tuple[
         if (np.array(d, dtype=np.float64) > 1).any():
             i = int(np.argmax(np.array(d, dtype=np.float64)))
             return False, f"{d[i]} ulp at {i}: got {g[i]!r} want {w[i]!r}", frac
+        return True, "", frac
+    if rule == "gemm32":
+        # tensor-core GEMM (bf16/f16 in, fp32 accumulate, one rounding to the
+        # output dtype) vs the reference's fp64 ascending-k sum: within one
+        # output ulp plus the fp32 accumulation bound k * 2^-23 * sum|a||b|
+        a, b = logical(case.inputs[0]), logical(case.inputs[1])
+        k = a.shape[1]
+        acc_bound = (k * 2.0 ** -23) * (np.abs(a) @ np.abs(b)).ravel()
+        wf = w.astype(np.float32)
+        ulp = np.spacing(np.abs(wf)).astype(np.float64) * (2.0 ** 16 if dtype == BF16 else 2.0 ** 13)
+        if dtype == F16:
+            ulp = np.spacing(np.abs(w.astype(np.float16))).astype(np.float64)
+        err = np.abs(g - w)
+        lim = ulp + acc_bound
+        if (err > lim).any() or np.isnan(err).any():
+            i = int(np.argmax(err - lim))
+            return False, f"err {err[i]:.3e} > bound {lim[i]:.3e} at {i}: got {g[i]!r} want {w[i]!r}", frac
         return True, "", frac
     tol = float(rule.split(":")[1])
     scale = np.maximum(1.0, np.abs(w))

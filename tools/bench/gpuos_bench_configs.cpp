@@ -275,7 +275,8 @@ int gb_config2(int device, int n_tasks, int steps, double* out) {
 }
 
 // out: [0] step us (median), [1] tasks/s, [2] GFLOP/s, [3] failed tasks,
-//      [4] max |o - ref| / max(1,|ref|) over head 0 (fp64 host reference)
+//      [4] max |o - ref| / max(1,|ref|) over head 0 (fp64 host reference),
+//      [5..8] median us of the scale / QK^T / softmax / PV phases
 int gb_config3(int device, int dtype, int steps, double* out) {
   const int H = 32, S = 128, D = 64;
   const DType dt = static_cast<DType>(dtype);
@@ -322,11 +323,13 @@ int gb_config3(int device, int dtype, int steps, double* out) {
   };
   const TensorView sc0 = view_of(scale, 0, {}, {});
   std::vector<double> step_us;
+  std::vector<double> phase_us[4];
   uint64_t failed = 0;
   std::vector<TaskHandle> hs;
   for (int s = 0; s < steps + 2; ++s) {
     const double t0 = now_ms();
     for (int phase = 0; phase < 4; ++phase) {
+      const double tp = now_ms();
       hs.clear();
       for (int h = 0; h < H; ++h) {
         switch (phase) {
@@ -344,6 +347,7 @@ int gb_config3(int device, int dtype, int steps, double* out) {
         th.wait();
         if (s >= 2) failed += th.state() == TaskState::Failed ? 1 : 0;
       }
+      if (s >= 2) phase_us[phase].push_back((now_ms() - tp) * 1e3);
     }
     if (s >= 2) step_us.push_back((now_ms() - t0) * 1e3);
   }
@@ -395,6 +399,10 @@ int gb_config3(int device, int dtype, int steps, double* out) {
   out[2] = flops / (med / 1e6) / 1e9;
   out[3] = static_cast<double>(failed);
   out[4] = err;
+  for (int ph = 0; ph < 4; ++ph) {  // [5..8] median us of scale / QK^T / softmax / PV phases
+    std::sort(phase_us[ph].begin(), phase_us[ph].end());
+    out[5 + ph] = phase_us[ph][phase_us[ph].size() / 2];
+  }
   return 0;
 }
 
