@@ -122,13 +122,53 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
   for (int k = 0; k < A; ++k) in[k] = (const T*)t->views[1 + k].addr;
   int64_t lo, hi;
   part_range(n, c->part, c->nparts, 1, &lo, &hi);
-  for (int64_t e = lo + c->tid; e < hi; e += c->nthreads) {
-    int64_t off[1 + A];
-    space_offsets(s, (uint32_t)e, off);
-    double x[A];
+  if (s.rank == 1) {
+    // one coalesced dimension (stride-k views, rank-0 / row broadcasts over a
+    // flat output): offsets are e * stride, no divmod, strides in registers
+    int64_t st[1 + A];
 #pragma unroll
-    for (int k = 0; k < A; ++k) x[k] = DT_<DT>::gload(in[k] + off[1 + k]);
-    DT_<DT>::store(out + off[0], f(x));
+    for (int k = 0; k <= A; ++k) st[k] = s.st[k][0];
+    constexpr int U1 = 8;
+    const int64_t step = (int64_t)c->nthreads * U1;
+    for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
+      double x[U1][A];
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) {
+#pragma unroll
+          for (int k = 0; k < A; ++k) x[u][k] = DT_<DT>::gload(in[k] + e * st[1 + k]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) DT_<DT>::store(out + e * st[0], f(x[u]));
+      }
+    }
+    return;
+  }
+  // U elements per thread per round, all loads issued before any use, so a
+  // round costs one memory latency instead of U
+  constexpr int U = 4;
+  const int64_t step = (int64_t)c->nthreads * U;
+  for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
+    int64_t off[U][1 + A];
+    double x[U][A];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * c->nthreads;
+      if (e < hi) {
+        space_offsets(s, (uint32_t)e, off[u]);
+#pragma unroll
+        for (int k = 0; k < A; ++k) x[u][k] = DT_<DT>::gload(in[k] + off[u][1 + k]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * c->nthreads;
+      if (e < hi) DT_<DT>::store(out + off[u][0], f(x[u]));
+    }
   }
 }
 

@@ -148,6 +148,69 @@ __device__ __forceinline__ double row_max_scan(int dt, const char* base, int64_t
 }
 
 // ---- softmax ----
+constexpr int kSoftmaxRegs = 8;  // rows of <= 256 elements stay in registers
+
+// Short rows of a 32/16-bit float dtype: one warp per row, the row held in
+// registers (one load round trip), dtype fixed at compile time.  The maximum
+// keeps the reference's scan semantics (NaN first element => NaN, otherwise
+// NaN-skipping, first extremum wins); exp runs in fp32 (expf, <= 2 ulp: the
+// argument x - max is exact in double and its float rounding moves p_i by at
+// most |d| e^d 2^-24 <= 2.2e-8), the sum in fp64, and the normalisation is a
+// multiply by the fp64 reciprocal -- within the rel 1e-6 / 1-ulp rules of
+// ops.hpp:200-238's fp64 computation (tests/cases.py row_cases).
+template <int DT>
+__device__ __noinline__ int softmax_rows_f(const gpuos_view& in, const gpuos_view& out, const RowIter& it,
+                                           const RowSched& rs, int64_t cols, int64_t si, int64_t so) {
+  typedef typename DT_<DT>::T T;
+  for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
+    int64_t oi, oo;
+    it.offsets(row, in.strides, out.strides, &oi, &oo);
+    const T* ib = (const T*)in.addr + oi;
+    T* ob = (T*)out.addr + oo;
+    float x[kSoftmaxRegs];
+#pragma unroll
+    for (int i = 0; i < kSoftmaxRegs; ++i) {
+      const int64_t j = rs.lane + 32 * i;
+      x[i] = j < cols ? (float)DT_<DT>::gload(ib + j * si) : 0.0f;
+    }
+    // (value, first index) maximum over the non-NaN elements
+    float mv = 0.0f;
+    int mi = -1;
+#pragma unroll
+    for (int i = 0; i < kSoftmaxRegs; ++i) {
+      const int j = rs.lane + 32 * i;
+      if (j < cols && x[i] == x[i] && (mi < 0 || mv < x[i])) {
+        mv = x[i];
+        mi = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
+      const int oi2 = __shfl_xor_sync(0xffffffffu, mi, o);
+      if (oi2 >= 0 && (mi < 0 || mv < ov || (!(ov < mv) && oi2 < mi))) {
+        mv = ov;
+        mi = oi2;
+      }
+    }
+    const float x0 = __shfl_sync(0xffffffffu, x[0], 0);
+    const double mx = (x0 != x0) ? (double)x0 : (double)mv;
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSoftmaxRegs; ++i) {
+      const int64_t j = rs.lane + 32 * i;
+      x[i] = j < cols ? expf((float)((double)x[i] - mx)) : 0.0f;
+      sum += (double)x[i];
+    }
+    const double inv = __drcp_rn(warp_sum(sum));
+#pragma unroll
+    for (int i = 0; i < kSoftmaxRegs; ++i) {
+      const int64_t j = rs.lane + 32 * i;
+      if (j < cols) DT_<DT>::store(ob + j * so, (double)x[i] * inv);
+    }
+  }
+  return GPUOS_OK;
+}
 __device__ __noinline__ int op_softmax(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
   const gpuos_view& out = t->views[0];
@@ -166,6 +229,13 @@ __device__ __noinline__ int op_softmax(const gpuos_task* t, const Ctx* c) {
   RowSched rs;
   rs.init(c, it.rows, cols);
   char* scratch = c->smem;
+  if (rs.per_warp && cols <= 32 * kSoftmaxRegs && dt != GPUOS_F64) {
+    switch (dt) {
+      case GPUOS_F32: return softmax_rows_f<GPUOS_F32>(in, out, it, rs, cols, si, so);
+      case GPUOS_F16: return softmax_rows_f<GPUOS_F16>(in, out, it, rs, cols, si, so);
+      default: return softmax_rows_f<GPUOS_BF16>(in, out, it, rs, cols, si, so);
+    }
+  }
   // whole-group units visit identical rows, so their barriers stay matched
   for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
     int64_t oi, oo;

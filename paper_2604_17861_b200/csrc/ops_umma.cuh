@@ -110,6 +110,101 @@ __device__ __forceinline__ uint32_t umma_elem_off(int row, int kk, int rows) {
   return (uint32_t)(((kk >> 3) * rows + row) * 16 + (kk & 7) * 2);
 }
 
+// Gather a `rows` x 64 operand chunk into the canonical layout: element
+// (r, kk) = src[(r0 + r) * s_r + (k0 + kk) * s_k], zero outside r < r_lim,
+// k0 + kk < k_lim.  K-contiguous sources move one 16-byte core-matrix row per
+// load; row-contiguous sources move eight rows of one k per load; anything
+// else goes element by element -- in every case eight independent loads per
+// thread are in flight before the first store.
+__device__ __forceinline__ void umma_stage(char* dst, int rows, const uint16_t* src, int64_t s_r, int64_t s_k,
+                                           int r0, int r_lim, int k0, int k_lim, const Ctx* c) {
+  const int nt = c->nthreads;
+  const bool base16 = ((uintptr_t)src & 15) == 0;
+  if (s_k == 1 && base16 && (s_r & 7) == 0) {
+    const int units = rows * (kUmmaKChunk / 8);
+    for (int u0 = c->tid; u0 < units; u0 += nt * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + q * nt;
+        v[q] = make_uint4(0, 0, 0, 0);
+        if (u < units) {
+          const int r = u >> 3, kc = u & 7;
+          const int gr = r0 + r, gk = k0 + 8 * kc;
+          if (gr < r_lim && gk + 8 <= k_lim) {
+            v[q] = __ldcg(reinterpret_cast<const uint4*>(src + gr * s_r + gk));
+          } else if (gr < r_lim && gk < k_lim) {
+            uint16_t h[8];
+            for (int i = 0; i < 8; ++i) h[i] = gk + i < k_lim ? __ldcg(src + gr * s_r + gk + i) : (uint16_t)0;
+            v[q] = make_uint4(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16), h[4] | ((uint32_t)h[5] << 16),
+                              h[6] | ((uint32_t)h[7] << 16));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + q * nt;
+        if (u < units) {
+          const int r = u >> 3, kc = u & 7;
+          *reinterpret_cast<uint4*>(dst + (kc * rows + r) * 16) = v[q];
+        }
+      }
+    }
+    return;
+  }
+  if (s_r == 1 && base16 && (s_k & 7) == 0) {
+    const int rg = rows / 8, units = rg * kUmmaKChunk;
+    for (int u0 = c->tid; u0 < units; u0 += nt * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + q * nt;
+        v[q] = make_uint4(0, 0, 0, 0);
+        if (u < units) {
+          const int g = u % rg, kk = u / rg;
+          const int gr = r0 + 8 * g, gk = k0 + kk;
+          if (gk < k_lim && gr + 8 <= r_lim) {
+            v[q] = __ldcg(reinterpret_cast<const uint4*>(src + gr + gk * s_k));
+          } else if (gk < k_lim && gr < r_lim) {
+            uint16_t h[8];
+            for (int i = 0; i < 8; ++i) h[i] = gr + i < r_lim ? __ldcg(src + gr + i + gk * s_k) : (uint16_t)0;
+            v[q] = make_uint4(h[0] | ((uint32_t)h[1] << 16), h[2] | ((uint32_t)h[3] << 16), h[4] | ((uint32_t)h[5] << 16),
+                              h[6] | ((uint32_t)h[7] << 16));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int u = u0 + q * nt;
+        if (u < units) {
+          const int g = u % rg, kk = u / rg;
+          const uint32_t w[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *(uint16_t*)(dst + umma_elem_off(8 * g + i, kk, rows)) = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+        }
+      }
+    }
+    return;
+  }
+  const int units = rows * kUmmaKChunk;
+  for (int u0 = c->tid; u0 < units; u0 += nt * 8) {
+    uint16_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int u = u0 + q * nt;
+      const int r = u / kUmmaKChunk, kk = u % kUmmaKChunk;
+      const int gr = r0 + r, gk = k0 + kk;
+      v[q] = (u < units && gr < r_lim && gk < k_lim) ? __ldcg(src + gr * s_r + gk * s_k) : (uint16_t)0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int u = u0 + q * nt;
+      if (u < units) *(uint16_t*)(dst + umma_elem_off(u / kUmmaKChunk, u % kUmmaKChunk, rows)) = v[q];
+    }
+  }
+}
+
 // out (m x n) = a (m x k) . b (k x n) for 16-bit float views, fp32 accumulate.
 // Requires Ctx::tmem (128 columns) and Ctx::mbar; 32 KB of scratch.
 __device__ int matmul_umma(const gpuos_view& a, const gpuos_view& b, const gpuos_view& out, int m, int k, int n,
@@ -140,20 +235,10 @@ __device__ int matmul_umma(const gpuos_view& a, const gpuos_view& b, const gpuos
     const int nmma = (nn + 15) & ~15;  // MMA N: multiple of 16
     const uint32_t idesc = umma_instr_desc(fmt, kUmmaM, nmma);
     for (int k0 = 0; k0 < k; k0 += kUmmaKChunk) {
-      // stage A chunk: rows i0.., cols k0.. (zero beyond m / k)
-      for (int e = c->tid; e < kUmmaM * kUmmaKChunk; e += nt) {
-        const int row = e / kUmmaKChunk, kk = e % kUmmaKChunk;
-        const int gi = i0 + row, gk = k0 + kk;
-        const uint16_t v = (gi < m && gk < k) ? __ldcg(ap + gi * sa0 + gk * sa1) : (uint16_t)0;
-        *(uint16_t*)(sA + umma_elem_off(row, kk, kUmmaM)) = v;
-      }
-      // stage B^T chunk: row j of the N x K operand = column j0+j of b
-      for (int e = c->tid; e < kUmmaN * kUmmaKChunk; e += nt) {
-        const int j = e % kUmmaN, kk = e / kUmmaN;
-        const int gj = j0 + j, gk = k0 + kk;
-        const uint16_t v = (gj < n && gk < k) ? __ldcg(bp + gk * sb0 + gj * sb1) : (uint16_t)0;
-        *(uint16_t*)(sB + umma_elem_off(j, kk, kUmmaN)) = v;
-      }
+      // stage A chunk (rows i0.., cols k0..) and B^T chunk (row j of the
+      // N x K operand = column j0+j of b), zero beyond m / n / k
+      umma_stage(sA, kUmmaM, ap, sa0, sa1, i0, m, k0, k, c);
+      umma_stage(sB, kUmmaN, bp, sb1, sb0, j0, n, k0, k, c);
       // generic-proxy smem writes -> visible to the tensor core's async proxy
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();

@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -230,6 +231,7 @@ RuntimeConfig bench_cfg(int device, size_t capacity) {
   cfg.capacity = capacity;
   cfg.telemetry_enabled = false;
   cfg.device_buffers = true;
+  if (const char* w = std::getenv("GB_WORKERS")) cfg.workers.num_workers = static_cast<size_t>(std::atoi(w));
   return cfg;
 }
 
