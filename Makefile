@@ -14,12 +14,18 @@ CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -I
 LIBDIR := paper_2604_17861_b200/lib
 CSRC := paper_2604_17861_b200/csrc
 OBJ := build/obj
-DEV_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dev_state.h include/gpuos_cuda.h
+DEV_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dev_state.h $(CSRC)/ring_format.h include/gpuos_cuda.h
 HOST_HDRS := $(wildcard paper_2604_17861_b200/include/gpuos/*.hpp) include/gpuos_cuda.h
 
 all: lib bench cpp-tests oracle
 
-lib: $(LIBDIR)/libgpuos_cuda.so
+lib: $(LIBDIR)/libgpuos_cuda.so $(LIBDIR)/gpuos_worker_rdc.cubin
+
+# relocatable image of the same worker: native injected operators are linked
+# against it at runtime (nvJitLink) into a new worker module
+$(LIBDIR)/gpuos_worker_rdc.cubin: $(CSRC)/worker.cu $(DEV_HDRS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -rdc=true -maxrregcount=80 -cubin $< -o $@
 bench: $(LIBDIR)/libgpuos_bench.so
 cpp-tests: build/cpp/test_runtime build/cpp/test_host
 

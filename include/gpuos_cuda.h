@@ -17,8 +17,23 @@
 #ifndef GPUOS_CUDA_H_
 #define GPUOS_CUDA_H_
 
+#ifdef __CUDACC_RTC__  /* NVRTC (natively compiled injected ops): no libc headers */
+#include <cuda/std/cstddef>
+#include <cuda/std/cstdint>
+typedef cuda::std::size_t size_t;
+typedef cuda::std::int8_t int8_t;
+typedef cuda::std::int16_t int16_t;
+typedef cuda::std::int32_t int32_t;
+typedef cuda::std::int64_t int64_t;
+typedef cuda::std::uint8_t uint8_t;
+typedef cuda::std::uint16_t uint16_t;
+typedef cuda::std::uint32_t uint32_t;
+typedef cuda::std::uint64_t uint64_t;
+typedef cuda::std::uintptr_t uintptr_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -371,6 +386,34 @@ int gpuos_copy_async(gpuos_dev* dev, void* dst, const void* src, uint64_t bytes,
 int gpuos_jit_compile(const char* src, const char* const* opts, int nopts, void** cubin,
                       size_t* size, uint64_t* compile_ns, uint64_t* link_ns, char* log, size_t logcap);
 void gpuos_free(void* p);
+
+/* ---------------- natively compiled injected operators ----------------
+ * The live injection path installs a verified device program (no module load,
+ * no kernel restart).  Promotion to native code: the op's program is turned
+ * into CUDA C++ by the host runtime, compiled by NVRTC to a relocatable
+ * sm_100a object, linked by nvJitLink with the relocatable worker image into
+ * a new worker module, and loaded at a generation handover (drain at a ticket
+ * boundary, load, relaunch; cuModuleLoadData blocks while a kernel is
+ * resident).  The table entry then names a native kind with the program kept
+ * as fallback (ModuleCache compile step, opcompiler.hpp:180-189). */
+#define GPUOS_NATIVE_SLOTS 32 /* natively compiled injected ops per device */
+typedef struct gpuos_native_stats {
+  uint64_t drain_ns;    /* sentinel published -> resident generation exited */
+  uint64_t load_ns;     /* cuModuleLoadData + symbol lookup + jit table write */
+  uint64_t relaunch_ns; /* new generation launched */
+} gpuos_native_stats;
+int gpuos_jit_compile_object(const char* src, void** obj, size_t* size, uint64_t* compile_ns, char* log,
+                             size_t logcap);
+int gpuos_jit_link_worker(const void* const* objs, const size_t* sizes, int n, void** cubin, size_t* size,
+                          uint64_t* link_ns, char* log, size_t logcap);
+/* `ptr_syms[i]` names a __device__ function-pointer variable of the module
+ * holding the native op for jit slot `slots[i]`. */
+int gpuos_dev_load_native(gpuos_dev* dev, const void* cubin, size_t size, const uint32_t* slots,
+                          const char* const* ptr_syms, int n, gpuos_native_stats* stats);
+/* Like gpuos_table_install_program, but the entry dispatches native jit slot
+ * `slot` (the program stays attached as the fallback body). */
+int gpuos_table_install_native(gpuos_dev* dev, uint32_t op_id, uint32_t slot, const gpuos_instr* code,
+                               uint32_t n_instr, int arity, int dtype, gpuos_inject_stats* stats);
 
 /* Human-readable name of an error code (errors.hpp:43-72). */
 const char* gpuos_error_name(int code);

@@ -32,6 +32,121 @@
 #include "ring_format.h"
 #include "gpuos_cuda.h"
 
+#include <dlfcn.h>
+namespace {
+struct JitApi {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*log)(nvrtcProgram, char*);
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*cubin)(nvrtcProgram, char*);
+  nvrtcResult (*destroy)(nvrtcProgram*);
+  nvJitLinkResult (*l_create)(nvJitLinkHandle*, uint32_t, const char**);
+  nvJitLinkResult (*l_add)(nvJitLinkHandle, nvJitLinkInputType, const void*, size_t, const char*);
+  nvJitLinkResult (*l_complete)(nvJitLinkHandle);
+  nvJitLinkResult (*l_err_size)(nvJitLinkHandle, size_t*);
+  nvJitLinkResult (*l_err)(nvJitLinkHandle, char*);
+  nvJitLinkResult (*l_cubin_size)(nvJitLinkHandle, size_t*);
+  nvJitLinkResult (*l_cubin)(nvJitLinkHandle, void*);
+  nvJitLinkResult (*l_destroy)(nvJitLinkHandle*);
+};
+
+void* open_first(const char* const* names) {
+  for (const char* const* n = names; *n; ++n)
+    if (void* h = dlopen(*n, RTLD_NOW | RTLD_LOCAL)) return h;
+  return nullptr;
+}
+
+JitApi load_jit() {
+  JitApi a;
+  static const char* rtc[] = {"/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12", nullptr};
+  static const char* lnk[] = {"/usr/local/cuda/lib64/libnvJitLink.so.12", "libnvJitLink.so.12", nullptr};
+  void* hr = open_first(rtc);
+  void* hl = open_first(lnk);
+  if (!hr || !hl) {
+    a.why = "cannot load libnvrtc/libnvJitLink";
+    return a;
+  }
+#define GPUOS_SYM(h, field, name)                       \
+  a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name)); \
+  if (!a.field) {                                       \
+    a.why = std::string("missing symbol ") + name;      \
+    return a;                                           \
+  }
+  GPUOS_SYM(hr, create, "nvrtcCreateProgram");
+  GPUOS_SYM(hr, compile, "nvrtcCompileProgram");
+  GPUOS_SYM(hr, log_size, "nvrtcGetProgramLogSize");
+  GPUOS_SYM(hr, log, "nvrtcGetProgramLog");
+  GPUOS_SYM(hr, cubin_size, "nvrtcGetCUBINSize");
+  GPUOS_SYM(hr, cubin, "nvrtcGetCUBIN");
+  GPUOS_SYM(hr, destroy, "nvrtcDestroyProgram");
+  GPUOS_SYM(hl, l_create, "__nvJitLinkCreate_12_9");
+  GPUOS_SYM(hl, l_add, "__nvJitLinkAddData_12_9");
+  GPUOS_SYM(hl, l_complete, "__nvJitLinkComplete_12_9");
+  GPUOS_SYM(hl, l_err_size, "__nvJitLinkGetErrorLogSize_12_9");
+  GPUOS_SYM(hl, l_err, "__nvJitLinkGetErrorLog_12_9");
+  GPUOS_SYM(hl, l_cubin_size, "__nvJitLinkGetLinkedCubinSize_12_9");
+  GPUOS_SYM(hl, l_cubin, "__nvJitLinkGetLinkedCubin_12_9");
+  GPUOS_SYM(hl, l_destroy, "__nvJitLinkDestroy_12_9");
+#undef GPUOS_SYM
+  a.ok = true;
+  return a;
+}
+
+const JitApi& jit_api() {
+  static const JitApi api = load_jit();
+  return api;
+}
+
+// CUDA driver entry points for module loading (dlopen'd like NVRTC, so the
+// library carries no link-time dependency on libcuda).
+struct DrvApi {
+  bool ok = false;
+  CUresult (*load)(CUmodule*, const void*);
+  CUresult (*unload)(CUmodule);
+  CUresult (*get_fn)(CUfunction*, CUmodule, const char*);
+  CUresult (*get_global)(CUdeviceptr*, size_t*, CUmodule, const char*);
+  CUresult (*fn_attr)(CUfunction, CUfunction_attribute, int);
+  CUresult (*dtoh)(void*, CUdeviceptr, size_t);
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                     void**, void**);
+};
+DrvApi load_drv() {
+  DrvApi a;
+  static const char* names[] = {"libcuda.so.1", "libcuda.so", nullptr};
+  void* h = open_first(names);
+  if (!h) return a;
+  a.load = reinterpret_cast<decltype(a.load)>(dlsym(h, "cuModuleLoadData"));
+  a.unload = reinterpret_cast<decltype(a.unload)>(dlsym(h, "cuModuleUnload"));
+  a.get_fn = reinterpret_cast<decltype(a.get_fn)>(dlsym(h, "cuModuleGetFunction"));
+  a.get_global = reinterpret_cast<decltype(a.get_global)>(dlsym(h, "cuModuleGetGlobal_v2"));
+  a.fn_attr = reinterpret_cast<decltype(a.fn_attr)>(dlsym(h, "cuFuncSetAttribute"));
+  a.dtoh = reinterpret_cast<decltype(a.dtoh)>(dlsym(h, "cuMemcpyDtoH_v2"));
+  a.launch = reinterpret_cast<decltype(a.launch)>(dlsym(h, "cuLaunchKernel"));
+  a.ok = a.load && a.unload && a.get_fn && a.get_global && a.fn_attr && a.dtoh && a.launch;
+  return a;
+}
+const DrvApi& drv_api() {
+  static const DrvApi api = load_drv();
+  return api;
+}
+
+// Directory holding this library (lib/), from which the native-injection
+// pipeline finds the relocatable worker image and the device headers.
+std::string lib_dir() {
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&jit_api), &info) && info.dli_fname) {
+    std::string p = info.dli_fname;
+    const size_t slash = p.rfind('/');
+    return slash == std::string::npos ? std::string(".") : p.substr(0, slash);
+  }
+  return ".";
+}
+}  // namespace
+
 using gdev::DevState;
 using gdev::TableEntry;
 
@@ -77,6 +192,9 @@ struct gpuos_dev {
   uint32_t workers = 0, threads = 0, smem = 0;
   std::atomic<bool> running{false};
   uint64_t resume_pos = 0;  // first ticket of the next worker generation
+  void* native_fn = nullptr;   // CUfunction of a JIT-linked worker module (null: the built-in one)
+  void* native_mod = nullptr;  // its CUmodule
+  void** jit_dev = nullptr;    // device array of kJitSlots native op pointers
   // table
   std::mutex table_mu;
   std::vector<TableEntry> bank[2];
@@ -221,8 +339,20 @@ static uint64_t tsc_to_ns(const gpuos_dev* d, uint64_t tsc) {
   return d->ns0 + (uint64_t)((double)(int64_t)(tsc - d->tsc0) / d->tsc_per_ns);
 }
 
-static int launch_workers(gpuos_dev* d) {
+static int launch_generation(gpuos_dev* d) {
+  if (d->native_fn) {
+    void* args[] = {&d->S};
+    if (drv_api().launch((CUfunction)d->native_fn, d->workers, 1, 1, gdev::worker_threads(), 1, 1, d->smem,
+                         (CUstream)d->ks, args, nullptr) != CUDA_SUCCESS)
+      return GPUOS_INTERNAL;
+    return GPUOS_OK;
+  }
   GPUOS_CK(gdev::launch_worker(d->S, d->workers, gdev::worker_threads(), d->smem, d->ks));
+  return GPUOS_OK;
+}
+
+static int launch_workers(gpuos_dev* d) {
+  if (const int rc = launch_generation(d)) return rc;
   note_resident(d->device, +1);
   d->running.store(true, std::memory_order_release);
   return GPUOS_OK;
@@ -321,6 +451,8 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   GPUOS_CK(cudaMalloc(&d->dtrace, d->trace_cap * sizeof(gdev::TraceRec)));
   GPUOS_CK(cudaMemsetAsync(d->dtrace, 0, d->trace_cap * sizeof(gdev::TraceRec), d->side));
   GPUOS_CK(cudaMalloc(&d->launch_counters, gdev::kLaunchCounters * 4));
+  GPUOS_CK(cudaMalloc(&d->jit_dev, gdev::kJitSlots * sizeof(void*)));
+  GPUOS_CK(cudaMemsetAsync(d->jit_dev, 0, gdev::kJitSlots * sizeof(void*), d->side));
   GPUOS_CK(cudaMemsetAsync(d->launch_counters, 0, gdev::kLaunchCounters * 4, d->side));
 
   DevState& s = d->shadow;
@@ -352,6 +484,7 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   s.dev_epoch = d->dev_epoch;
   s.trace = d->dtrace;
   s.trace_cap = d->trace_cap;
+  s.jit_fns = reinterpret_cast<gdev::OpFn_*>(d->jit_dev);
   GPUOS_CK(cudaMemcpyAsync(d->S, &s, sizeof(s), cudaMemcpyHostToDevice, d->side));
   GPUOS_CK(cudaStreamSynchronize(d->side));
 
@@ -435,7 +568,7 @@ int gpuos_dev_run_finite(gpuos_dev* d, float* kernel_ms) {
   GPUOS_CK(cudaEventCreate(&e0));
   GPUOS_CK(cudaEventCreate(&e1));
   GPUOS_CK(cudaEventRecord(e0, d->ks));
-  GPUOS_CK(gdev::launch_worker(d->S, d->workers, gdev::worker_threads(), d->smem, d->ks));
+  if (const int lrc = launch_generation(d)) return lrc;
   GPUOS_CK(cudaEventRecord(e1, d->ks));
   GPUOS_CK(cudaStreamSynchronize(d->ks));
   float ms = 0;
@@ -453,7 +586,8 @@ int gpuos_dev_close(gpuos_dev* d) {
   cudaSetDevice(d->device);
   cudaStreamSynchronize(d->side);
   Grave g;
-  g.dev = {d->S, d->dbank[0], d->dbank[1], d->dev_epoch, d->dtrace, d->launch_counters};
+  g.dev = {d->S, d->dbank[0], d->dbank[1], d->dev_epoch, d->dtrace, d->launch_counters, (void*)d->jit_dev};
+  if (d->native_mod) drv_api().unload((CUmodule)d->native_mod);
   g.dev.insert(g.dev.end(), d->dev_blocks.begin(), d->dev_blocks.end());
   g.managed = d->managed_blocks;
   g.pinned = d->pinned_blocks;
@@ -962,6 +1096,46 @@ int gpuos_table_install_builtin(gpuos_dev* d, uint32_t op_id, uint32_t kind) {
   return table_mutate(d, op_id, e, nullptr);
 }
 
+static int install_program_kind(gpuos_dev* d, uint32_t op_id, uint32_t kind, const gpuos_instr* code,
+                                uint32_t n_instr, int arity, int dtype, int maxd, gpuos_inject_stats* st);
+
+// Structural verification of a program (bytecode.hpp:142-201 restated);
+// returns the max stack depth or -1.
+static int verify_program(const gpuos_instr* code, uint32_t n_instr, int arity) {
+  int depth = 0, maxd = 0;
+  for (uint32_t i = 0; i < n_instr; ++i) {
+    const int op = code[i].op;
+    if (op == GPUOS_BC_PUSH_CONST || op == GPUOS_BC_LOAD_IN) {
+      if (op == GPUOS_BC_LOAD_IN && (code[i].k < 0 || code[i].k >= arity)) return -1;
+      ++depth;
+    } else if (op == GPUOS_BC_ADD || op == GPUOS_BC_SUB || op == GPUOS_BC_MUL || op == GPUOS_BC_DIV ||
+               op == GPUOS_BC_MAX || op == GPUOS_BC_MIN) {
+      if (depth < 2) return -1;
+      --depth;
+    } else if (op == GPUOS_BC_STORE_OUT) {
+      if (i + 1 != n_instr || depth != 1) return -1;
+      --depth;
+    } else if (op > GPUOS_BC_STORE_OUT) {
+      return -1;
+    } else if (depth < 1) {
+      return -1;
+    }
+    maxd = std::max(maxd, depth);
+  }
+  return maxd > GPUOS_MAX_STACK ? -1 : maxd;
+}
+
+int gpuos_table_install_native(gpuos_dev* d, uint32_t op_id, uint32_t slot, const gpuos_instr* code,
+                               uint32_t n_instr, int arity, int dtype, gpuos_inject_stats* st) {
+  if (!d || !code) return GPUOS_INTERNAL;
+  if (op_id >= d->cfg.table_slots || slot >= gdev::kJitSlots) return GPUOS_OUT_OF_RANGE;
+  if (n_instr == 0 || n_instr > GPUOS_MAX_PROGRAM) return GPUOS_VERIFY_ERROR;
+  if (arity < 0 || arity > GPUOS_MAX_INPUTS) return GPUOS_ARITY_ERROR;
+  const int maxd = verify_program(code, n_instr, arity);
+  if (maxd < 0) return GPUOS_VERIFY_ERROR;
+  return install_program_kind(d, op_id, gdev::kJitKindBase + slot, code, n_instr, arity, dtype, maxd, st);
+}
+
 int gpuos_table_install_program(gpuos_dev* d, uint32_t op_id, const gpuos_instr* code, uint32_t n_instr,
                                 int arity, int dtype, gpuos_inject_stats* st) {
   if (!d || !code) return GPUOS_INTERNAL;
@@ -990,6 +1164,11 @@ int gpuos_table_install_program(gpuos_dev* d, uint32_t op_id, const gpuos_instr*
     maxd = std::max(maxd, depth);
   }
   if (maxd > GPUOS_MAX_STACK) return GPUOS_VERIFY_ERROR;
+  return install_program_kind(d, op_id, GPUOS_KIND_PROGRAM, code, n_instr, arity, dtype, maxd, st);
+}
+
+static int install_program_kind(gpuos_dev* d, uint32_t op_id, uint32_t kind, const gpuos_instr* code,
+                                uint32_t n_instr, int arity, int dtype, int maxd, gpuos_inject_stats* st) {
   cudaSetDevice(d->device);
   const uint64_t t0 = steady_ns();
   const size_t bytes = sizeof(gdev::ProgramHeader) + n_instr * sizeof(gpuos_instr);
@@ -1007,7 +1186,7 @@ int gpuos_table_install_program(gpuos_dev* d, uint32_t op_id, const gpuos_instr*
   }
   const uint64_t t1 = steady_ns();
   TableEntry e{};
-  e.kind = GPUOS_KIND_PROGRAM;
+  e.kind = (uint16_t)kind;
   e.status = 1;
   e.aux = (uint64_t)p;
   const int rc = table_mutate(d, op_id, e, st);
@@ -1113,6 +1292,7 @@ static uint32_t parts_for(const gpuos_dev* d, const gpuos_task* t, uint32_t kind
   int64_t n = 1;
   for (int i = 0; i < o.rank; ++i) n *= o.extents[i];
   int64_t p = 1;
+  if (kind >= gdev::kJitKindBase && kind < gdev::kJitKindBase + gdev::kJitSlots) kind = GPUOS_KIND_PROGRAM;
   switch (kind) {
     case GPUOS_OP_ADD: case GPUOS_OP_MUL: case GPUOS_OP_RELU: case GPUOS_OP_GELU: case GPUOS_KIND_PROGRAM:
       p = (n + 2047) / 2048;
@@ -1255,77 +1435,6 @@ int gpuos_copy_async(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, i
 // Loaded on first use with dlopen(RTLD_LOCAL) from the CUDA toolkit this
 // library was built against, so a different libnvJitLink/libnvrtc already in
 // the process (e.g. one bundled with PyTorch) cannot shadow the 12.9 symbols.
-}  // extern "C"
-#include <dlfcn.h>
-namespace {
-struct JitApi {
-  bool ok = false;
-  std::string why;
-  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
-  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
-  nvrtcResult (*log_size)(nvrtcProgram, size_t*);
-  nvrtcResult (*log)(nvrtcProgram, char*);
-  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*);
-  nvrtcResult (*cubin)(nvrtcProgram, char*);
-  nvrtcResult (*destroy)(nvrtcProgram*);
-  nvJitLinkResult (*l_create)(nvJitLinkHandle*, uint32_t, const char**);
-  nvJitLinkResult (*l_add)(nvJitLinkHandle, nvJitLinkInputType, const void*, size_t, const char*);
-  nvJitLinkResult (*l_complete)(nvJitLinkHandle);
-  nvJitLinkResult (*l_err_size)(nvJitLinkHandle, size_t*);
-  nvJitLinkResult (*l_err)(nvJitLinkHandle, char*);
-  nvJitLinkResult (*l_cubin_size)(nvJitLinkHandle, size_t*);
-  nvJitLinkResult (*l_cubin)(nvJitLinkHandle, void*);
-  nvJitLinkResult (*l_destroy)(nvJitLinkHandle*);
-};
-
-void* open_first(const char* const* names) {
-  for (const char* const* n = names; *n; ++n)
-    if (void* h = dlopen(*n, RTLD_NOW | RTLD_LOCAL)) return h;
-  return nullptr;
-}
-
-JitApi load_jit() {
-  JitApi a;
-  static const char* rtc[] = {"/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12", nullptr};
-  static const char* lnk[] = {"/usr/local/cuda/lib64/libnvJitLink.so.12", "libnvJitLink.so.12", nullptr};
-  void* hr = open_first(rtc);
-  void* hl = open_first(lnk);
-  if (!hr || !hl) {
-    a.why = "cannot load libnvrtc/libnvJitLink";
-    return a;
-  }
-#define GPUOS_SYM(h, field, name)                       \
-  a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name)); \
-  if (!a.field) {                                       \
-    a.why = std::string("missing symbol ") + name;      \
-    return a;                                           \
-  }
-  GPUOS_SYM(hr, create, "nvrtcCreateProgram");
-  GPUOS_SYM(hr, compile, "nvrtcCompileProgram");
-  GPUOS_SYM(hr, log_size, "nvrtcGetProgramLogSize");
-  GPUOS_SYM(hr, log, "nvrtcGetProgramLog");
-  GPUOS_SYM(hr, cubin_size, "nvrtcGetCUBINSize");
-  GPUOS_SYM(hr, cubin, "nvrtcGetCUBIN");
-  GPUOS_SYM(hr, destroy, "nvrtcDestroyProgram");
-  GPUOS_SYM(hl, l_create, "__nvJitLinkCreate_12_9");
-  GPUOS_SYM(hl, l_add, "__nvJitLinkAddData_12_9");
-  GPUOS_SYM(hl, l_complete, "__nvJitLinkComplete_12_9");
-  GPUOS_SYM(hl, l_err_size, "__nvJitLinkGetErrorLogSize_12_9");
-  GPUOS_SYM(hl, l_err, "__nvJitLinkGetErrorLog_12_9");
-  GPUOS_SYM(hl, l_cubin_size, "__nvJitLinkGetLinkedCubinSize_12_9");
-  GPUOS_SYM(hl, l_cubin, "__nvJitLinkGetLinkedCubin_12_9");
-  GPUOS_SYM(hl, l_destroy, "__nvJitLinkDestroy_12_9");
-#undef GPUOS_SYM
-  a.ok = true;
-  return a;
-}
-
-const JitApi& jit_api() {
-  static const JitApi api = load_jit();
-  return api;
-}
-}  // namespace
-extern "C" {
 
 int gpuos_jit_compile(const char* src, const char* const* opts, int nopts, void** cubin, size_t* size,
                       uint64_t* compile_ns, uint64_t* link_ns, char* log, size_t logcap) {
@@ -1388,5 +1497,170 @@ int gpuos_jit_compile(const char* src, const char* const* opts, int nopts, void*
 }
 
 void gpuos_free(void* p) { std::free(p); }
+// ---------------------------------------------------------------- native injected operators
+
+// NVRTC only: CUDA source -> relocatable sm_100a object, with the device
+// headers (csrc/, include/) and the toolkit headers on the include path and
+// GPUOS_JIT_TU defined (the builtin entry points stay in the worker image).
+int gpuos_jit_compile_object(const char* src, void** obj, size_t* size, uint64_t* compile_ns, char* log,
+                             size_t logcap) {
+  if (!src || !obj || !size) return GPUOS_INTERNAL;
+  auto put_log = [&](const std::string& m) {
+    if (log && logcap) std::snprintf(log, logcap, "%s", m.c_str());
+  };
+  const JitApi& J = jit_api();
+  if (!J.ok) {
+    put_log(J.why);
+    return GPUOS_INTERNAL;
+  }
+  const std::string dir = lib_dir();
+  const std::string inc_csrc = "-I" + dir + "/../csrc", inc_abi = "-I" + dir + "/../../include";
+  const char* cuda_home = std::getenv("CUDA_HOME");
+  const std::string inc_cuda = std::string("-I") + (cuda_home ? cuda_home : "/usr/local/cuda") + "/include";
+  const uint64_t t0 = steady_ns();
+  nvrtcProgram prog;
+  if (J.create(&prog, src, "gpuos_native_op.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return GPUOS_INTERNAL;
+  // register cap = the image's (-maxrregcount=80 in the Makefile): rdc callees must fit every caller
+  const char* o[] = {"-arch=sm_100a", "-rdc=true", "--fmad=false", "-std=c++17", "-default-device", "--maxrregcount=80",
+                     "-DGPUOS_JIT_TU=1", inc_csrc.c_str(), inc_abi.c_str(), inc_cuda.c_str()};
+  if (J.compile(prog, (int)(sizeof(o) / sizeof(o[0])), o) != NVRTC_SUCCESS) {
+    size_t n = 0;
+    J.log_size(prog, &n);
+    std::string l(n, '\0');
+    J.log(prog, l.data());
+    put_log(l);
+    J.destroy(&prog);
+    return GPUOS_SYNTAX_ERROR;
+  }
+  size_t n = 0;
+  J.cubin_size(prog, &n);
+  void* out = std::malloc(n);
+  J.cubin(prog, static_cast<char*>(out));
+  J.destroy(&prog);
+  *obj = out;
+  *size = n;
+  if (compile_ns) *compile_ns = steady_ns() - t0;
+  return GPUOS_OK;
+}
+
+// nvJitLink: the relocatable worker image (lib/gpuos_worker_rdc.cubin, built
+// from the same worker.cu) + native op objects -> one loadable sm_100a cubin.
+int gpuos_jit_link_worker(const void* const* objs, const size_t* sizes, int n, void** cubin, size_t* size,
+                          uint64_t* link_ns, char* log, size_t logcap) {
+  if (!cubin || !size || n < 0 || (n > 0 && (!objs || !sizes))) return GPUOS_INTERNAL;
+  auto put_log = [&](const std::string& m) {
+    if (log && logcap) std::snprintf(log, logcap, "%s", m.c_str());
+  };
+  const JitApi& J = jit_api();
+  if (!J.ok) {
+    put_log(J.why);
+    return GPUOS_INTERNAL;
+  }
+  static std::vector<char> image;
+  static std::mutex image_mu;
+  {
+    std::lock_guard<std::mutex> lk(image_mu);
+    if (image.empty()) {
+      const std::string path = lib_dir() + "/gpuos_worker_rdc.cubin";
+      FILE* f = std::fopen(path.c_str(), "rb");
+      if (!f) {
+        put_log("missing " + path);
+        return GPUOS_IO_ERROR;
+      }
+      std::fseek(f, 0, SEEK_END);
+      const long len = std::ftell(f);
+      std::fseek(f, 0, SEEK_SET);
+      image.resize((size_t)len);
+      const size_t got = std::fread(image.data(), 1, image.size(), f);
+      std::fclose(f);
+      if (got != image.size()) {
+        image.clear();
+        return GPUOS_IO_ERROR;
+      }
+    }
+  }
+  const uint64_t t0 = steady_ns();
+  nvJitLinkHandle h;
+  const char* lopts[] = {"-arch=sm_100a"};
+  if (J.l_create(&h, 1, lopts) != NVJITLINK_SUCCESS) return GPUOS_INTERNAL;
+  bool ok = J.l_add(h, NVJITLINK_INPUT_CUBIN, image.data(), image.size(), "gpuos_worker") == NVJITLINK_SUCCESS;
+  for (int i = 0; ok && i < n; ++i)
+    ok = J.l_add(h, NVJITLINK_INPUT_CUBIN, objs[i], sizes[i], "gpuos_native_op") == NVJITLINK_SUCCESS;
+  if (!ok || J.l_complete(h) != NVJITLINK_SUCCESS) {
+    size_t ln = 0;
+    J.l_err_size(h, &ln);
+    std::string l(ln, '\0');
+    J.l_err(h, l.data());
+    put_log(l);
+    J.l_destroy(&h);
+    return GPUOS_VERIFY_ERROR;
+  }
+  size_t cs = 0;
+  J.l_cubin_size(h, &cs);
+  void* out = std::malloc(cs);
+  J.l_cubin(h, out);
+  J.l_destroy(&h);
+  *cubin = out;
+  *size = cs;
+  if (link_ns) *link_ns = steady_ns() - t0;
+  return GPUOS_OK;
+}
+
+// Generation handover onto a JIT-linked worker module: drain the resident
+// generation at a ticket boundary (sentinel, FIFO), load the module (a module
+// load needs an idle context: measured, profiles/r01_probe2_*.log), publish
+// its native op pointers to the device jit table, relaunch.  The ring,
+// tables, buffers and counters carry over; no published task is lost.
+int gpuos_dev_load_native(gpuos_dev* d, const void* cubin, size_t size, const uint32_t* slots,
+                          const char* const* ptr_syms, int n, gpuos_native_stats* st) {
+  if (!d || !cubin || size == 0 || n < 0 || (n > 0 && (!slots || !ptr_syms))) return GPUOS_INTERNAL;
+  const DrvApi& D = drv_api();
+  if (!D.ok) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  const bool was_running = d->running.load(std::memory_order_acquire);
+  const uint64_t t0 = steady_ns();
+  if (was_running) {
+    const int rc = gpuos_dev_stop(d);
+    if (rc) return rc;
+  }
+  const uint64_t t1 = steady_ns();
+  CUmodule mod = nullptr;
+  if (D.load(&mod, cubin) != CUDA_SUCCESS) return GPUOS_VERIFY_ERROR;
+  CUfunction fn = nullptr;
+  if (D.get_fn(&fn, mod, "gpuos_worker_kernel") != CUDA_SUCCESS) {
+    D.unload(mod);
+    return GPUOS_VERIFY_ERROR;
+  }
+  D.fn_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)d->smem);
+  D.fn_attr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
+  std::vector<void*> table(gdev::kJitSlots, nullptr);
+  for (int i = 0; i < n; ++i) {
+    CUdeviceptr gp = 0;
+    size_t gs = 0;
+    if (slots[i] >= gdev::kJitSlots || D.get_global(&gp, &gs, mod, ptr_syms[i]) != CUDA_SUCCESS || gs != 8 ||
+        D.dtoh(&table[slots[i]], gp, 8) != CUDA_SUCCESS) {
+      D.unload(mod);
+      return GPUOS_VERIFY_ERROR;
+    }
+  }
+  GPUOS_CK(cudaMemcpyAsync(d->jit_dev, table.data(), table.size() * sizeof(void*), cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  if (d->native_mod) D.unload((CUmodule)d->native_mod);
+  d->native_mod = mod;
+  d->native_fn = fn;
+  const uint64_t t2 = steady_ns();
+  if (was_running) {
+    const int rc = gpuos_dev_start(d);
+    if (rc) return rc;
+  }
+  const uint64_t t3 = steady_ns();
+  if (st) {
+    st->drain_ns = t1 - t0;
+    st->load_ns = t2 - t1;
+    st->relaunch_ns = t3 - t2;
+  }
+  return GPUOS_OK;
+}
+
 
 }  // extern "C"

@@ -5,10 +5,13 @@
 // for strided addressing, and system/gpu-scope memory primitives.
 #pragma once
 
+#include "gpuos_cuda.h"  // fixed-width types (NVRTC-safe)
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 #include "gpuos_cuda.h"
 

@@ -3,8 +3,10 @@
 // entry, the device trace record, and the launch helpers worker.cu exports.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 #include "gpuos_cuda.h"
 
@@ -14,6 +16,12 @@ constexpr uint32_t kMaxWorkers = 2048;
 constexpr uint64_t kQuiescent = ~0ull;  // EpochRegistry::kQuiescent (optable.hpp:62)
 constexpr uint64_t kRunning = ~0ull;    // stop_pos while running
 constexpr uint32_t kNumKinds = 80;      // module jump-table slots
+// Natively compiled injected operators (NVRTC + nvJitLink, linked into a
+// worker module at a generation handover): kinds [kJitKindBase, +kJitSlots)
+// dispatch through DevState::jit_fns; a generation without that code falls
+// back to the entry's device program (TableEntry::aux).
+constexpr uint32_t kJitKindBase = 96;
+constexpr uint32_t kJitSlots = 32;
 constexpr uint32_t kTaskBytes = 384;
 constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
 constexpr uint32_t kHeaderBytes = 5120;  // worker: task buffers, control blocks, counters, entry cache
@@ -38,6 +46,8 @@ struct ProgramHeader {
   int32_t dtype;
   int32_t max_stack;
 };
+
+typedef void* OpFn_;  // device function pointer (OpFn) as stored in HBM
 
 struct TraceRec {  // Tracepoint (telemetry.hpp:22-32) plus a publication stamp
   uint64_t stamp;  // ticket*2+2 once complete
@@ -95,8 +105,10 @@ struct alignas(128) DevState {
   uint64_t* dev_epoch;        // same, in HBM
   TraceRec* trace;
   uint64_t trace_cap;
+  OpFn_* jit_fns;  // kJitSlots entries, filled by the host after loading a native module (null = none)
 };
 
+#ifndef __CUDACC_RTC__
 // ---- host-callable helpers implemented in worker.cu ----
 void load_all_kernels(int* worker_regs, size_t* worker_local);
 cudaError_t launch_worker(DevState* s, uint32_t workers, uint32_t threads, uint32_t smem, cudaStream_t st);
@@ -106,5 +118,7 @@ cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st);
 uint32_t worker_smem_bytes();
 uint32_t worker_threads();
 cudaError_t worker_occupancy(int* per_sm);
+
+#endif  // __CUDACC_RTC__
 
 }  // namespace gdev

@@ -267,10 +267,12 @@ __device__ __forceinline__ int ew_entry(const gpuos_task* t, const Ctx* c, bool 
   return ew_general<F>(t, c, allow_int);
 }
 
+#ifndef GPUOS_JIT_TU  // a natively compiled injected op links against these; it must not redefine them
 __device__ __noinline__ int op_add(const gpuos_task* t, const Ctx* c) { return ew_entry<FAdd>(t, c, true); }
 __device__ __noinline__ int op_mul(const gpuos_task* t, const Ctx* c) { return ew_entry<FMul>(t, c, true); }
 __device__ __noinline__ int op_relu(const gpuos_task* t, const Ctx* c) { return ew_entry<FRelu>(t, c, true); }
 __device__ __noinline__ int op_gelu(const gpuos_task* t, const Ctx* c) { return ew_general<FGelu>(t, c, false); }
+#endif
 
 // ---------------------------------------------------------------------------
 // Injected operators: a verified stack-machine program evaluated in double per
@@ -336,6 +338,7 @@ __device__ void program_loop(const gpuos_task* t, const Ctx* c, const Space& s, 
   }
 }
 
+#ifndef GPUOS_JIT_TU
 // Checks in load_module's order (opcompiler.hpp:72-101).
 __device__ __noinline__ int op_program(const gpuos_task* t, const Ctx* c) {
   const ProgramHeader* hp = (const ProgramHeader*)c->aux;
@@ -423,6 +426,45 @@ __device__ __noinline__ int op_kv_append(const gpuos_task* t, const Ctx* c) {
     store_any(dt, (char*)kc.addr, ko, load_any(dt, (const char*)nk.addr, no));
     store_any(dt, (char*)vc.addr, vo, load_any(dt, (const char*)nv.addr, mo));
   }
+  return GPUOS_OK;
+}
+
+#endif  // GPUOS_JIT_TU
+
+// ---------------------------------------------------------------------------
+// Natively compiled injected operators: the host generates a functor F from
+// the verified program (straight-line code, same fp64 operations in the same
+// order, one rounding on store) and instantiates jit_body<F, DT> in an NVRTC
+// translation unit.  Checks in op_program's order (opcompiler.hpp:72-101), so
+// a promoted op returns exactly what its device program returns.
+// ---------------------------------------------------------------------------
+template <class F, int DT>
+__device__ __forceinline__ int jit_body(const gpuos_task* t, const Ctx* c) {
+  constexpr int A = F::A;
+  if (t->n_inputs != A) return GPUOS_ARITY_ERROR;
+  const gpuos_view& out = t->views[0];
+  if (out.dtype != DT) return GPUOS_DTYPE_MISMATCH;
+  const int64_t n = numel(out);
+  if (n == 0) return GPUOS_OK;
+  if (n >= (int64_t)1 << 31) return GPUOS_TOO_LARGE;
+  F f;
+  if (c->flags & kPlanDenseSame) {
+    ew_dense<DT>(t, c, n, f);
+    return GPUOS_OK;
+  }
+  int64_t st[A > 0 ? A : 1][GPUOS_MAX_RANK];
+  for (int k = 0; k < A; ++k) {
+    if (t->views[1 + k].dtype != out.dtype) return GPUOS_DTYPE_MISMATCH;
+    if (!broadcast_strides(t->views[1 + k], out, st[k])) return GPUOS_INCOMPATIBLE_SHAPES;
+    const int b = bind_code(t->views[1 + k]);
+    if (b) return b;
+  }
+  const int b = bind_code(out);
+  if (b) return b;
+  Space s;
+  build_space(s, out, A, st);
+  if (s.dense) ew_dense<DT>(t, c, n, f);
+  else ew_strided<DT>(t, c, s, n, f);
   return GPUOS_OK;
 }
 

@@ -251,7 +251,9 @@ __device__ __forceinline__ void resolve(DevState* S, const WConst& K, uint32_t w
     }
     break;
   }
-  const uint32_t kind = e.kind < kNumKinds ? e.kind : (uint32_t)GPUOS_KIND_KILLED;
+  const uint32_t kind = (e.kind < kNumKinds || (e.kind >= kJitKindBase && e.kind < kJitKindBase + kJitSlots))
+                            ? e.kind
+                            : (uint32_t)GPUOS_KIND_KILLED;
   ctl->code = code;
   ctl->kind = kind;
   ctl->aux = e.aux;
@@ -650,6 +652,7 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   ctx.smem_bytes = scratch;
   ctx.aux = 0;
   ctx.flags = 0;
+  OpFn_* const jit_fns = S->jit_fns;
   ctx.tmem = H->tmem_base + (uint32_t)(g * (kTmemCols / kGroups));
   ctx.mbar = &H->mbar[g];
   ctx.mma_phase = &H->mma_phase[g];
@@ -672,7 +675,16 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
     if (code == GPUOS_OK) {
       ctx.aux = ctl->aux;
       ctx.flags = task->flags | ctl->plan;
-      const OpFn fn = g_kind_fns[ctl->kind];
+      const uint32_t kind = ctl->kind;
+      OpFn fn;
+      if (kind < kNumKinds) {
+        fn = g_kind_fns[kind];
+      } else {
+        // native injected op, or its device program when this generation's
+        // module does not carry the native code
+        OpFn_ p = jit_fns ? jit_fns[kind - kJitKindBase] : nullptr;
+        fn = p ? reinterpret_cast<OpFn>(p) : op_program;
+      }
       code = fn(task, &ctx);
     }
     group_sync(&ctx);
@@ -786,6 +798,7 @@ __global__ void gpuos_clock_probe(uint64_t* out) { out[0] = globaltimer(); }
 typedef void (*TaskKernel)(const gpuos_task, uint64_t, uint32_t*);
 
 static TaskKernel task_kernel_for(uint32_t kind) {
+  if (kind >= kJitKindBase && kind < kJitKindBase + kJitSlots) kind = GPUOS_KIND_PROGRAM;
   switch (kind) {
     case GPUOS_OP_ADD: return gpuos_task_kernel<GPUOS_OP_ADD>;
     case GPUOS_OP_MUL: return gpuos_task_kernel<GPUOS_OP_MUL>;

@@ -93,6 +93,19 @@ class OperatorTable {
     return st;
   }
 
+  /// Point op_id at native jit slot `slot` of the resident worker module
+  /// (the program stays attached as fallback body); one version bump.
+  gpuos_inject_stats install_native(uint32_t op_id, uint32_t slot, const Bytecode& code, int arity, DType dtype,
+                                    InjectionRecord meta = {}) {
+    const std::vector<gpuos_instr> img = to_device_program(code);
+    gpuos_inject_stats st{};
+    check_abi(gpuos_table_install_native(dev_, op_id, slot, img.data(), static_cast<uint32_t>(img.size()), arity,
+                                         static_cast<int>(dtype), &st),
+              "install native");
+    record(op_id, std::move(meta));
+    return st;
+  }
+
   /// Fail-fast stub under a new version; no audit record (optable.hpp:135-142).
   void kill(uint32_t op_id) {
     if (op_id >= slots_) throw Error(ErrorCode::OutOfRange, "op id " + std::to_string(op_id) + " out of range");

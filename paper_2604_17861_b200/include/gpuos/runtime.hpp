@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <span>
 #include <string>
@@ -472,6 +473,90 @@ class Runtime {
   /// Timings of the most recent injection's upload / epoch wait / bank write / flip.
   const gpuos_inject_stats& last_inject_stats() const { return last_inject_; }
 
+  /// Phases of the most recent native promotion (ns).
+  struct NativeStats {
+    uint64_t codegen_ns = 0, compile_ns = 0, link_ns = 0;
+    gpuos_native_stats handover{};  // drain / module load / relaunch
+    gpuos_inject_stats install{};   // table flip
+    bool compiled = false;          // false: the object came from the native cache
+  };
+  const NativeStats& last_native_stats() const { return last_native_; }
+
+  /// Promote injected operator `op_id` from its device program to native
+  /// code: CUDA C++ generated from the verified program (same fp64 operations
+  /// in the same order, one rounding on store), NVRTC -> relocatable sm_100a
+  /// object (cached per signature), nvJitLink with the relocatable worker
+  /// image and every other promoted op, module load at a generation handover,
+  /// then a dual-bank flip of the entry to the native kind.  Throws
+  /// gpuos::Error on compile/link/load failures; the op keeps running its
+  /// program until the flip.
+  void promote_native(uint32_t op_id) {
+    if (stopped_) throw Error(ErrorCode::RuntimeStopped, "promote after shutdown");
+    auto it = modules_by_id_.find(op_id);
+    if (it == modules_by_id_.end()) throw Error(ErrorCode::NotInstalled, "op " + std::to_string(op_id) + " is not injected");
+    const ModulePtr mod = it->second;
+    NativeStats st;
+    uint32_t slot;
+    if (auto sl = native_slot_.find(op_id); sl != native_slot_.end()) {
+      slot = sl->second;
+    } else {
+      if (native_slot_.size() >= GPUOS_NATIVE_SLOTS) throw Error(ErrorCode::TableFull, "no free native slots");
+      slot = static_cast<uint32_t>(native_slot_.size());
+      native_slot_[op_id] = slot;
+    }
+    const std::string key = signature_key(mod->signature);
+    auto obj = native_cache_.find(key);
+    if (obj == native_cache_.end()) {
+      const uint64_t t0 = monotonic_ns();
+      const std::string src = native_source(mod->bytecode, mod->signature.arity, mod->signature.dtype, key);
+      const uint64_t t1 = monotonic_ns();
+      void* o = nullptr;
+      size_t n = 0;
+      uint64_t cns = 0;
+      std::string log(16384, '\0');
+      const int rc = gpuos_jit_compile_object(src.c_str(), &o, &n, &cns, log.data(), log.size());
+      if (rc != 0) throw Error(static_cast<ErrorCode>(rc), "native compile failed: " + std::string(log.c_str()));
+      obj = native_cache_.emplace(key, std::string(static_cast<const char*>(o), n)).first;
+      gpuos_free(o);
+      st.codegen_ns = t1 - t0;
+      st.compile_ns = cns;
+      st.compiled = true;
+    }
+    native_obj_[slot] = key;
+    // link the worker image with every promoted op's object
+    std::vector<const void*> objs;
+    std::vector<size_t> sizes;
+    std::vector<uint32_t> slots;
+    std::vector<std::string> syms;
+    for (const auto& [s_, k_] : native_obj_) {
+      const std::string& bytes = native_cache_.at(k_);
+      objs.push_back(bytes.data());
+      sizes.push_back(bytes.size());
+      slots.push_back(s_);
+      syms.push_back(native_symbol(k_));
+    }
+    void* cubin = nullptr;
+    size_t csize = 0;
+    std::string log(16384, '\0');
+    int rc = gpuos_jit_link_worker(objs.data(), sizes.data(), static_cast<int>(objs.size()), &cubin, &csize,
+                                   &st.link_ns, log.data(), log.size());
+    if (rc != 0) throw Error(static_cast<ErrorCode>(rc), "native link failed: " + std::string(log.c_str()));
+    std::vector<const char*> sym_ptrs;
+    for (const std::string& x : syms) sym_ptrs.push_back(x.c_str());
+    rc = gpuos_dev_load_native(dev_, cubin, csize, slots.data(), sym_ptrs.data(), static_cast<int>(slots.size()),
+                               &st.handover);
+    gpuos_free(cubin);
+    if (rc != 0) throw Error(static_cast<ErrorCode>(rc), "native module load failed");
+    InjectionRecord meta;
+    meta.template_name = mod->signature.template_name;
+    meta.params.assign(mod->signature.params.begin(), mod->signature.params.end());
+    meta.signature = key + " [native]";
+    st.install = table_->install_native(op_id, slot, mod->bytecode, mod->signature.arity, mod->signature.dtype,
+                                        std::move(meta));
+    last_native_ = st;
+  }
+  bool is_native(uint32_t op_id) const { return native_slot_.count(op_id) != 0; }
+
   TemplateRegistry& templates() { return registry_; }
   OperatorTable& table() { return *table_; }
   ModuleCache& module_cache() { return cache_; }
@@ -828,6 +913,98 @@ class Runtime {
   uint64_t next_injected_id_ = kFirstInjectedId;
   std::unordered_map<uint32_t, ModulePtr> modules_by_id_;
   gpuos_inject_stats last_inject_{};
+  // native promotion: op id -> jit slot, slot -> signature key, key -> object
+  std::unordered_map<uint32_t, uint32_t> native_slot_;
+  std::map<uint32_t, std::string> native_obj_;
+  std::unordered_map<std::string, std::string> native_cache_;
+  NativeStats last_native_{};
+
+  static std::string native_symbol(const std::string& key) {
+    uint64_t h = 1469598103934665603ull;  // FNV-1a of the signature key
+    for (const unsigned char ch : key) h = (h ^ ch) * 1099511628211ull;
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "gpuos_native_ptr_%016llx", static_cast<unsigned long long>(h));
+    return buf;
+  }
+
+  /// CUDA C++ for one verified program: the stack machine unrolled into
+  /// straight-line fp64 code with exactly the interpreter's operations
+  /// (ops_elementwise.cuh run_program), wrapped in jit_body.
+  static std::string native_source(const Bytecode& code, int arity, DType dtype, const std::string& key) {
+    const std::string sym = native_symbol(key);
+    const std::string tag = sym.substr(std::string("gpuos_native_ptr_").size());
+    std::string body;
+    std::vector<std::string> st;
+    int tmp = 0;
+    char line[160];
+    auto fresh = [&]() { return "t" + std::to_string(tmp++); };
+    for (const Instr& in : code) {
+      std::string r;
+      switch (in.op) {
+        case OpCode::PushConst: {
+          uint64_t bits;
+          std::memcpy(&bits, &in.value, 8);
+          r = fresh();
+          std::snprintf(line, sizeof(line), "    const double %s = __longlong_as_double(0x%016llxll);\n", r.c_str(),
+                        static_cast<unsigned long long>(bits));
+          break;
+        }
+        case OpCode::LoadIn:
+          r = fresh();
+          std::snprintf(line, sizeof(line), "    const double %s = v[%d];\n", r.c_str(), in.k);
+          break;
+        case OpCode::StoreOut:
+          std::snprintf(line, sizeof(line), "    return %s;\n", st.back().c_str());
+          body += line;
+          continue;
+        case OpCode::Add: case OpCode::Sub: case OpCode::Mul: case OpCode::Div: case OpCode::Max: case OpCode::Min: {
+          const std::string b = st.back();
+          st.pop_back();
+          const std::string a = st.back();
+          st.pop_back();
+          r = fresh();
+          const char* fn = in.op == OpCode::Add ? "__dadd_rn" : in.op == OpCode::Sub ? "__dsub_rn"
+                         : in.op == OpCode::Mul ? "__dmul_rn" : "__ddiv_rn";
+          if (in.op == OpCode::Max)
+            std::snprintf(line, sizeof(line), "    const double %s = %s < %s ? %s : %s;\n", r.c_str(), a.c_str(), b.c_str(),
+                          b.c_str(), a.c_str());
+          else if (in.op == OpCode::Min)
+            std::snprintf(line, sizeof(line), "    const double %s = %s < %s ? %s : %s;\n", r.c_str(), b.c_str(), a.c_str(),
+                          b.c_str(), a.c_str());
+          else
+            std::snprintf(line, sizeof(line), "    const double %s = %s(%s, %s);\n", r.c_str(), fn, a.c_str(), b.c_str());
+          break;
+        }
+        default: {  // unary
+          const std::string a = st.back();
+          st.pop_back();
+          r = fresh();
+          switch (in.op) {
+            case OpCode::Neg: std::snprintf(line, sizeof(line), "    const double %s = -%s;\n", r.c_str(), a.c_str()); break;
+            case OpCode::Exp: std::snprintf(line, sizeof(line), "    const double %s = exp(%s);\n", r.c_str(), a.c_str()); break;
+            case OpCode::Tanh: std::snprintf(line, sizeof(line), "    const double %s = tanh(%s);\n", r.c_str(), a.c_str()); break;
+            case OpCode::Abs: std::snprintf(line, sizeof(line), "    const double %s = fabs(%s);\n", r.c_str(), a.c_str()); break;
+            case OpCode::Sqrt: std::snprintf(line, sizeof(line), "    const double %s = __dsqrt_rn(%s);\n", r.c_str(), a.c_str()); break;
+            default:  // Narrow
+              std::snprintf(line, sizeof(line), "    const double %s = narrow_any(%d, %s);\n", r.c_str(), in.k, a.c_str());
+          }
+        }
+      }
+      body += line;
+      st.push_back(r);
+    }
+    std::string src;
+    src += "// generated by gpuos::Runtime::promote_native for signature: " + key + "\n";
+    src += "#include \"ops_elementwise.cuh\"\n";
+    src += "namespace gdev {\nstruct NativeF_" + tag + " {\n  static constexpr int A = " + std::to_string(arity) +
+           ";\n  __device__ __forceinline__ double operator()(const double* v) const {\n    (void)v;\n" + body +
+           "  }\n};\n}  // namespace gdev\n";
+    src += "extern \"C\" __device__ __noinline__ int gpuos_native_op_" + tag +
+           "(const gpuos_task* t, const gdev::Ctx* c) {\n  return gdev::jit_body<gdev::NativeF_" + tag + ", " +
+           std::to_string(static_cast<int>(dtype)) + ">(t, c);\n}\n";
+    src += "extern \"C\" __device__ gdev::OpFn " + sym + " = gpuos_native_op_" + tag + ";\n";
+    return src;
+  }
   mutable std::mutex trace_mu_;
   std::vector<Tracepoint> inline_trace_;
 };

@@ -512,6 +512,75 @@ TEST_CASE("hot swap under load: every row is entirely one variant, no canary hit
               st.upload_ns / 1e3, st.epoch_wait_ns / 1e3, st.bank_write_ns / 1e3, st.flip_ns / 1e3, old_rows, new_rows);
 }
 
+TEST_CASE("native promotion: NVRTC + nvJitLink op, generation handover, bit-identical to the program") {
+  Runtime rt(small_config(4096, 0));
+  std::mt19937_64 rng(909);
+  const double pa[2] = {1.5, -0.25};
+  // every shipped template, f32 and f64: the native code must return exactly
+  // what the device program returns (and what eval_expr + narrow gives)
+  const std::vector<std::string> names = rt.templates().names();
+  struct Op {
+    uint64_t id;
+    int arity;
+    DType dt;
+  };
+  std::vector<Op> ops;
+  for (const std::string& name : names)
+    for (DType dt : {DType::F32, DType::F64}) {
+      const OperatorTemplate t = rt.templates().get(name);
+      const double params[8] = {0.75, 2.5, 0, 0, 0, 0, 0, 0};
+      ops.push_back({rt.inject_operator(name, params, dt), t.arity, dt});
+    }
+  const uint64_t sa = rt.inject_operator("scale_add", pa);
+  ops.push_back({sa, 1, DType::F32});
+  const int64_t n = 3000;  // ragged: not a multiple of the vector width
+  std::vector<std::vector<TensorView>> ins(ops.size());
+  std::vector<TensorView> out_prog, out_nat;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    for (int k = 0; k < ops[i].arity; ++k) {
+      ins[i].push_back(rt.alloc_tensor(ops[i].dt, {n}));
+      fill(rt, ins[i].back(), random_vals(rng, static_cast<size_t>(n), -3.0, 3.0));
+    }
+    out_prog.push_back(rt.alloc_tensor(ops[i].dt, {n}));
+    out_nat.push_back(rt.alloc_tensor(ops[i].dt, {n}));
+    REQUIRE(rt.wait(rt.submit(ops[i].id, ins[i], out_prog[i])) == TaskState::Done);
+  }
+  double compile_ms = 0, link_ms = 0, handover_us = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    rt.promote_native(static_cast<uint32_t>(ops[i].id));
+    const auto& st = rt.last_native_stats();
+    compile_ms += st.compile_ns / 1e6;
+    link_ms = st.link_ns / 1e6;
+    handover_us = (st.handover.drain_ns + st.handover.load_ns + st.handover.relaunch_ns) / 1e3;
+    REQUIRE(rt.is_native(static_cast<uint32_t>(ops[i].id)));
+  }
+  REQUIRE(rt.worker_alive());
+  for (size_t i = 0; i < ops.size(); ++i) {
+    REQUIRE(rt.wait(rt.submit(ops[i].id, ins[i], out_nat[i])) == TaskState::Done);
+    REQUIRE(read_all(rt, out_nat[i]) == read_all(rt, out_prog[i]));
+  }
+  // strided + broadcast operands through the native body
+  auto bx = rt.alloc_tensor(DType::F32, {8, 64});
+  fill(rt, bx, random_vals(rng, 8 * 64));
+  TensorView row = bx;
+  row.shape = {1, 64};
+  row.strides = {64, 1};
+  auto bo = rt.alloc_tensor(DType::F32, {16, 64});
+  REQUIRE(rt.wait(rt.submit(sa, {row}, bo)) == TaskState::Done);
+  const auto xv = read_all(rt, bx);
+  const auto bov = read_all(rt, bo);
+  for (int r = 0; r < 16; ++r)
+    for (int c = 0; c < 64; ++c) REQUIRE(bov[static_cast<size_t>(r * 64 + c)] == f32(xv[static_cast<size_t>(c)] * 1.5 + -0.25));
+  // errors keep the program's codes
+  auto o64 = rt.alloc_tensor(DType::F64, {n});
+  auto he = rt.submit(sa, {ins.back()[0]}, o64);
+  REQUIRE(rt.wait(he) == TaskState::Failed);
+  CHECK(he.error() == ErrorCode::DTypeMismatch);
+  CHECK(rt.canary_hits() == 0);
+  std::printf("  native: %zu ops, nvrtc %.1f ms total, last nvJitLink %.1f ms, last handover %.1f us\n", ops.size(),
+              compile_ms, link_ms, handover_us);
+}
+
 TEST_CASE("shutdown drains every committed task") {
   Runtime rt(small_config(1024, 0));
   auto x = rt.alloc_tensor(DType::F32, {256});
