@@ -25,7 +25,7 @@ lib: $(LIBDIR)/libgpuos_cuda.so $(LIBDIR)/gpuos_worker_rdc.cubin
 # against it at runtime (nvJitLink) into a new worker module
 $(LIBDIR)/gpuos_worker_rdc.cubin: $(CSRC)/worker.cu $(DEV_HDRS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -rdc=true -maxrregcount=80 -cubin $< -o $@
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -rdc=true -maxrregcount=80 -DGPUOS_WORKER_IMAGE -cubin $< -o $@
 bench: $(LIBDIR)/libgpuos_bench.so
 cpp-tests: build/cpp/test_runtime build/cpp/test_host
 

@@ -198,6 +198,16 @@ def run_configs(lib, local: int) -> dict:
         "window_rows_checked": int(out[6]), "rows_not_one_variant": int(out[7]),
         "old_rows_past_window": int(out[8]), "failed_tasks": int(out[9]), "canary_hits": int(out[10]),
         "old_rows": int(out[11]), "new_rows": int(out[12])}
+    lib.gb_native.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_native(local, 200_000, out)
+    res["config4_native_promotion"] = {
+        "workload": "200,000 fp32 4096-element scale_add(1.5,-0.25) tasks as a device program, then promoted to "
+                    "native code (NVRTC -> relocatable sm_100a -> nvJitLink with the worker image -> module load at a "
+                    "generation handover) and run again",
+        "program_tasks_per_s": out[0], "native_tasks_per_s": out[1],
+        "promotion_ms": {"codegen": out[2], "nvrtc": out[3], "nvjitlink": out[4]},
+        "handover_us": {"drain": out[5], "module_load": out[6], "relaunch": out[7], "table_flip": out[8]},
+        "output_mismatches_native_vs_program": int(out[9])}
     return res
 
 

@@ -697,6 +697,7 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
   }
 }
 
+#ifndef GPUOS_WORKER_IMAGE  // the relocatable image for native ops carries only the worker
 // ---------------------------------------------------------------------------
 // Conventional path: the same bodies as standalone kernels, one launch per task.
 // ---------------------------------------------------------------------------
@@ -868,5 +869,7 @@ cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st) {
   gpuos_clock_probe<<<1, 1, 0, st>>>(out);
   return cudaGetLastError();
 }
+
+#endif  // GPUOS_WORKER_IMAGE
 
 }  // namespace gdev

@@ -504,4 +504,61 @@ int gb_config4(int device, int n_tasks, double* out) {
   return 0;
 }
 
+// Native promotion of an injected operator (config 4, second half): a stream
+// of 4096-element fp32 scale_add tasks run as a device program, then the op
+// is promoted to native code (NVRTC + nvJitLink + generation handover) and
+// the same stream runs again.
+// out: [0] program tasks/s, [1] native tasks/s, [2] codegen ms, [3] nvrtc ms,
+//      [4] nvJitLink ms, [5] drain us, [6] module load us, [7] relaunch us,
+//      [8] table flip us, [9] output mismatches native vs program
+int gb_native(int device, int n_tasks, double* out) {
+  const int64_t E = 4096;
+  const int kRows = 2048;
+  Runtime rt(bench_cfg(device, 4096));
+  const double pa[2] = {1.5, -0.25};
+  const uint32_t id = static_cast<uint32_t>(rt.inject_operator("scale_add", pa));
+  TensorView IN = rt.alloc_tensor(DType::F32, {int64_t{kRows} * E});
+  TensorView OA = rt.alloc_tensor(DType::F32, {int64_t{kRows} * E});
+  TensorView OB = rt.alloc_tensor(DType::F32, {int64_t{kRows} * E});
+  std::vector<float> x(static_cast<size_t>(kRows) * E);
+  std::mt19937_64 rng(config_seed(42, 4));
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  for (float& f : x) f = static_cast<float>(u(rng));
+  rt.pool().upload(IN.buffer, x.data(), x.size() * 4);
+  rt.wait_all();
+  check_abi(gpuos_dev_stop(rt.device()), "stop");
+  Events ev(rt.device());
+  auto stream = [&](const TensorView& O) {
+    return ev.generation([&] {
+      for (int t = 0; t < n_tasks; ++t) {
+        const int64_t r = t % kRows;
+        rt.submit(static_cast<uint64_t>(id), {view_of(IN, r * E, {E}, {1})}, view_of(O, r * E, {E}, {1}));
+      }
+      rt.wait_all();
+    });
+  };
+  stream(OA);  // warm
+  const double ms_prog = stream(OA);
+  rt.promote_native(id);  // workers stopped: the handover only loads + records the module
+  const auto& st = rt.last_native_stats();
+  stream(OB);  // warm
+  const double ms_nat = stream(OB);
+  std::vector<float> a(x.size()), b(x.size());
+  rt.pool().download(OA.buffer, a.data(), a.size() * 4);
+  rt.pool().download(OB.buffer, b.data(), b.size() * 4);
+  uint64_t bad = 0;
+  for (size_t i = 0; i < a.size(); ++i) bad += std::memcmp(&a[i], &b[i], 4) != 0;
+  out[0] = n_tasks / (ms_prog / 1e3);
+  out[1] = n_tasks / (ms_nat / 1e3);
+  out[2] = st.codegen_ns / 1e6;
+  out[3] = st.compile_ns / 1e6;
+  out[4] = st.link_ns / 1e6;
+  out[5] = st.handover.drain_ns / 1e3;
+  out[6] = st.handover.load_ns / 1e3;
+  out[7] = st.handover.relaunch_ns / 1e3;
+  out[8] = (st.install.upload_ns + st.install.epoch_wait_ns + st.install.bank_write_ns + st.install.flip_ns) / 1e3;
+  out[9] = static_cast<double>(bad);
+  return 0;
+}
+
 }  // extern "C"
