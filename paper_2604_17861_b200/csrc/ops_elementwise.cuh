@@ -41,7 +41,7 @@ struct FGelu {
 };
 
 // ---- the shared elementwise driver ----
-template <int DT, class F>
+template <int DT, class F, int U = 4>
 __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int64_t n, F f) {
   typedef typename DT_<DT>::T T;
   constexpr int A = F::A;
@@ -53,7 +53,6 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
 #pragma unroll
   for (int k = 0; k < A; ++k) aligned = aligned && (((uintptr_t)in[k] & 15) == 0);
   constexpr int V = 16 / sizeof(T);
-  constexpr int U = 4;
   int64_t tail_lo = 0;
   if (aligned) {
     const int64_t nv = n / V;
@@ -260,6 +259,8 @@ __device__ __forceinline__ int ew_entry(const gpuos_task* t, const Ctx* c, bool 
     const int64_t n = numel(t->views[0]);
     if (n > 0 && n < ((int64_t)1 << 31)) {
       F f;
+      // (U=8 would make a 4096-element task one round trip on a 128-thread
+      // group, but spills under the worker's register cap: measured slower)
       ew_dense<GPUOS_F32>(t, c, n, f);
       return GPUOS_OK;
     }

@@ -31,7 +31,7 @@ def summarize(name, ph, t_host=None):
 
 
 n = 4096
-with abi.Device(0, telemetry=True) as d:
+with abi.Device(0, telemetry=True, num_workers=int(os.environ.get("LP_WORKERS", "0"))) as d:
     a, b, c = d.alloc(abi.F32, n), d.alloc(abi.F32, n), d.alloc(abi.F32, n)
     a.write(np.ones(n, np.float32))
     b.write(np.ones(n, np.float32))
