@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 using namespace gpuos;
@@ -49,6 +50,37 @@ int main(int argc, char** argv) {
   }
   rt.wait_all();
   check_abi(gpuos_dev_stop(rt.device()), "stop");
+  // PW_OP=matmul_bf16: n bf16 matmul tasks (128x64 . 64x128, K as a
+  // transposed view) for tensor-pipe evidence instead of config-1 adds
+  const char* pw = std::getenv("PW_OP");
+  if (pw && std::string(pw) == "matmul_bf16") {
+    const int64_t M = 128, K = 64, N = 128;
+    const int nb = 256;  // distinct operand sets, reused round robin
+    TensorView QA = rt.alloc_tensor(DType::BF16, {int64_t{nb} * M * K});
+    TensorView KB = rt.alloc_tensor(DType::BF16, {int64_t{nb} * N * K});
+    TensorView OS = rt.alloc_tensor(DType::BF16, {int64_t{n} * M * N});
+    for (int r = 0; r < reps; ++r) {
+      for (int i = 0; i < n; ++i) {
+        TensorView a2 = QA, b2 = KB, o2 = OS;
+        a2.shape = {M, K};
+        a2.strides = {K, 1};
+        a2.offset = int64_t(i % nb) * M * K;
+        b2.shape = {K, N};
+        b2.strides = {1, K};
+        b2.offset = int64_t(i % nb) * N * K;
+        o2.shape = {M, N};
+        o2.strides = {N, 1};
+        o2.offset = int64_t(i) * M * N;
+        rt.submit(OpKind::MatMulSmall, {a2, b2}, o2);
+      }
+      float ms = 0;
+      check_abi(gpuos_dev_run_finite(rt.device(), &ms), "run_finite");
+      const double flops = 2.0 * M * N * K * n;
+      std::printf("{\"tasks\": %d, \"op\": \"matmul_bf16 128x64x128\", \"kernel_ms\": %.4f, \"tasks_per_s\": %.1f, "
+                  "\"TFLOPs\": %.3f}\n", n, ms, n / (ms / 1e3), flops / (ms / 1e3) / 1e12);
+    }
+    return 0;
+  }
   for (int r = 0; r < reps; ++r) {
     for (int i = 0; i < n; ++i) rt.submit(OpKind::Add, {a[i], b[i]}, c[i]);
     float ms = 0;
