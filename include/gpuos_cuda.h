@@ -109,6 +109,13 @@ enum gpuos_op_kind {
 #define GPUOS_FLAG_FUSED_COMPOSITE 0x1u
 #define GPUOS_FLAG_SHUTDOWN 0x2u
 #define GPUOS_FLAG_UNCAPPED 0x4u /* matmul/vecmat without the 256 cap (inline path, runtime.hpp:589-594) */
+/* A GPUOS_FLAG_FUSED_COMPOSITE task (op id GPUOS_COMPOSITE_OP_ID) carries, in
+ * scalars[0], the bits of the device address of its fused program (see
+ * gpuos_program_upload) and, in scalars[1], the bits of the device address of
+ * a completion record in mapped pinned memory: { n, cell_0, seq_0, ...,
+ * cell_{n-1}, seq_{n-1} } for the chain's earlier steps, completed together
+ * with the task's own done_cell (runtime.hpp:764-908). */
+#define GPUOS_MAX_FUSED 15
 
 /* Per-view bind status, resolved on the host at submit and surfaced by the
  * task body at the point where the reference constructs BoundView
@@ -328,6 +335,10 @@ int gpuos_table_install_builtin(gpuos_dev* dev, uint32_t op_id, uint32_t kind);
 /* Install an injected elementwise program (upload + dual-bank flip, no kernel restart). */
 int gpuos_table_install_program(gpuos_dev* dev, uint32_t op_id, const gpuos_instr* code,
                                 uint32_t n_instr, int arity, int dtype, gpuos_inject_stats* stats);
+/* Upload a verified elementwise program for per-task use (fused composites):
+ * returns its device address; programs live for the runtime's lifetime. */
+int gpuos_program_upload(gpuos_dev* dev, const gpuos_instr* code, uint32_t n_instr, int arity, int dtype,
+                         uint64_t* device_addr);
 /* Fail-fast stub under a new version (optable.hpp:135-142). */
 int gpuos_table_kill(gpuos_dev* dev, uint32_t op_id);
 

@@ -99,7 +99,7 @@ EXPORTS = [
     "gpuos_abi_version", "gpuos_default_cfg", "gpuos_dev_open", "gpuos_dev_close", "gpuos_dev_alive",
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
     "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_ring_submit_dense", "gpuos_event_done", "gpuos_jit_compile_object", "gpuos_jit_link_worker",
-    "gpuos_dev_load_native", "gpuos_table_install_native", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
+    "gpuos_dev_load_native", "gpuos_table_install_native", "gpuos_program_upload", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
     "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
     "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
@@ -144,6 +144,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                    C.c_char_p, C.c_size_t], I),
         "gpuos_dev_load_native": ([P, P, C.c_size_t, P, P, I, P], I),
         "gpuos_table_install_native": ([P, C.c_uint32, C.c_uint32, P, C.c_uint32, I, I, P], I),
+        "gpuos_program_upload": ([P, P, C.c_uint32, I, I, C.POINTER(C.c_uint64)], I),
         "gpuos_dev_clock_offset": ([P, C.POINTER(C.c_int64)], I),
         "gpuos_buf_alloc": ([P, I, U64, C.POINTER(U64), C.POINTER(P)], I),
         "gpuos_buf_free": ([P, U64], I),

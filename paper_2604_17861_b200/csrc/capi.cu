@@ -1167,6 +1167,31 @@ int gpuos_table_install_program(gpuos_dev* d, uint32_t op_id, const gpuos_instr*
   return install_program_kind(d, op_id, GPUOS_KIND_PROGRAM, code, n_instr, arity, dtype, maxd, st);
 }
 
+int gpuos_program_upload(gpuos_dev* d, const gpuos_instr* code, uint32_t n_instr, int arity, int dtype,
+                         uint64_t* device_addr) {
+  if (!d || !code || !device_addr) return GPUOS_INTERNAL;
+  if (n_instr == 0 || n_instr > GPUOS_MAX_PROGRAM) return GPUOS_VERIFY_ERROR;
+  if (arity < 0 || arity > GPUOS_MAX_INPUTS) return GPUOS_ARITY_ERROR;
+  const int maxd = verify_program(code, n_instr, arity);
+  if (maxd < 0) return GPUOS_VERIFY_ERROR;
+  cudaSetDevice(d->device);
+  const size_t bytes = sizeof(gdev::ProgramHeader) + n_instr * sizeof(gpuos_instr);
+  std::vector<char> img(bytes);
+  gdev::ProgramHeader h{n_instr, arity, dtype, maxd};
+  std::memcpy(img.data(), &h, sizeof(h));
+  std::memcpy(img.data() + sizeof(h), code, n_instr * sizeof(gpuos_instr));
+  void* p = nullptr;
+  GPUOS_CK(cudaMalloc(&p, bytes));
+  GPUOS_CK(cudaMemcpyAsync(p, img.data(), bytes, cudaMemcpyHostToDevice, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  {
+    std::lock_guard<std::mutex> lk(d->buf_mu);
+    d->dev_blocks.push_back(p);
+  }
+  *device_addr = (uint64_t)p;
+  return GPUOS_OK;
+}
+
 static int install_program_kind(gpuos_dev* d, uint32_t op_id, uint32_t kind, const gpuos_instr* code,
                                 uint32_t n_instr, int arity, int dtype, int maxd, gpuos_inject_stats* st) {
   cudaSetDevice(d->device);
@@ -1330,10 +1355,16 @@ int gpuos_launch_task(gpuos_dev* d, const gpuos_task* t, void* stream) {
   if (e.status == 0) return GPUOS_NOT_INSTALLED;
   if (e.status == 2) return GPUOS_OPERATOR_KILLED;
   cudaSetDevice(d->device);
-  const uint32_t nparts = parts_for(d, t, e.kind);
+  uint32_t kind = e.kind;
+  uint64_t aux = e.aux;
+  if (t->flags & GPUOS_FLAG_FUSED_COMPOSITE) {  // fused chain: its own program (scalars[0])
+    kind = GPUOS_KIND_PROGRAM;
+    std::memcpy(&aux, &t->scalars[0], 8);
+  }
+  const uint32_t nparts = parts_for(d, t, kind);
   uint32_t* counter = d->launch_counters + (d->launch_seq.fetch_add(1, std::memory_order_relaxed) % gdev::kLaunchCounters);
   cudaStream_t st = stream ? (cudaStream_t)stream : d->side;
-  GPUOS_CK(gdev::launch_task(t, e.kind, e.aux, nparts, counter, st));
+  GPUOS_CK(gdev::launch_task(t, kind, aux, nparts, counter, st));
   return GPUOS_OK;
 }
 

@@ -515,6 +515,12 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
                 if (ver != F.my_epoch) ver = stable_snapshot(S, K, w, ver);
                 F.my_epoch = ver;
                 resolve(S, K, w, H, task->op_id, ver, F.my_epoch, ctl);
+                if ((task->flags & GPUOS_FLAG_FUSED_COMPOSITE) && ctl->code == GPUOS_OK) {
+                  // fused elementwise chain (runtime.hpp:912-933): the entry at
+                  // the composite id gates it; the program rides in scalars[0]
+                  ctl->kind = GPUOS_KIND_PROGRAM;
+                  ctl->aux = (uint64_t)__double_as_longlong(task->scalars[0]);
+                }
                 ctl->version = ver;
                 ctl->t_deq = globaltimer();
               }
@@ -562,6 +568,19 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHea
   if (task->done_cell) {
     const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
     st_relaxed_sys((uint64_t*)task->done_cell, word);
+  }
+  if ((task->flags & GPUOS_FLAG_FUSED_COMPOSITE) && task->n_scalars > 1) {
+    // the chain's earlier steps complete with the composite: their (cell,
+    // seq) pairs sit in a host-written record (scalars[1])
+    const uint64_t* rec = (const uint64_t*)__double_as_longlong(task->scalars[1]);
+    if (rec) {
+      const uint64_t nsteps = ld_relaxed_sys(rec);
+      for (uint64_t k = 0; k < nsteps && k < GPUOS_MAX_FUSED; ++k) {
+        const uint64_t cell = ld_relaxed_sys(rec + 1 + 2 * k), seq = ld_relaxed_sys(rec + 2 + 2 * k);
+        const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (seq << 16);
+        st_relaxed_sys((uint64_t*)cell, word);
+      }
+    }
   }
   *(volatile uint64_t*)&H->done = H->done + 1;
   atomicAdd((unsigned long long*)&S->processed, 1ull);

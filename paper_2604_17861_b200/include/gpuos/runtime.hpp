@@ -65,6 +65,37 @@ inline uint64_t monotonic_ns() {
 
 namespace detail {
 
+/// Dataflow key of an expression (runtime.hpp:92-126's role): fused chains
+/// with different dataflow never share a compiled program.  Prefix form;
+/// constants print with 17 significant digits, so distinct values differ.
+inline void canonical_expr(const Expr& e, std::string& out) {
+  char buf[48];
+  switch (e.kind) {
+    case ExprKind::Const:
+      std::snprintf(buf, sizeof(buf), "c%.17g", e.value);
+      out += buf;
+      return;
+    case ExprKind::In:
+      out += "i" + std::to_string(e.index);
+      return;
+    case ExprKind::Param:
+      out += "p" + std::to_string(e.index);
+      return;
+    case ExprKind::Narrow:
+      out += "nw" + std::to_string(static_cast<int>(e.narrow_dtype));
+      break;
+    default:
+      out += std::to_string(static_cast<int>(e.kind));
+  }
+  out += '(';
+  if (e.a) canonical_expr(*e.a, out);
+  if (e.b) {
+    out += ',';
+    canonical_expr(*e.b, out);
+  }
+  out += ')';
+}
+
 /// Completion cells: 8-byte words in mapped pinned memory, one per live task,
 /// written exactly once (device st.release.sys, or the host on the inline and
 /// validation paths).  Replaces HandleState (runtime.hpp:59-88).  Reference
@@ -77,6 +108,19 @@ class CellPool {
   explicit CellPool(gpuos_dev* dev) : dev_(dev) { grow(); }
 
   uint64_t* word(uint32_t g) const { return blocks_[g >> kBlockBits].host + (g & (kBlock - 1)); }
+
+  /// Completion record of cell g for fused composites (mapped pinned, 32
+  /// words: n, then (cell device address, seq) pairs); allocated per block
+  /// on first use.  Only the composite's final cell owns one, and a cell is
+  /// not reused before its task completes, so records never race.
+  static constexpr uint32_t kRecordWords = 32;
+  uint64_t* record(uint32_t g, uint64_t* device_addr) {
+    Block& b = blocks_[g >> kBlockBits];
+    if (!b.rec_host) check_abi(gpuos_cells_alloc(dev_, kBlock * kRecordWords, &b.rec_host, &b.rec_dev), "records");
+    const uint64_t i = g & (kBlock - 1);
+    *device_addr = b.rec_dev + 8ull * kRecordWords * i;
+    return b.rec_host + kRecordWords * i;
+  }
   uint64_t device_addr(uint32_t g) const { return blocks_[g >> kBlockBits].dev + 8ull * (g & (kBlock - 1)); }
 
   /// Producer thread only.  A cell is reusable when no handle references it
@@ -154,6 +198,8 @@ class CellPool {
     uint64_t dev = 0;
     std::atomic<uint32_t>* refs = nullptr;
     uint64_t* last_seq = nullptr;  // seq of the cell's latest task, 0 = never used
+    uint64_t* rec_host = nullptr;  // fused-composite completion records (lazily)
+    uint64_t rec_dev = 0;
     bool heap = false;
   };
   void grow() {
@@ -413,24 +459,49 @@ class Runtime {
     }
     counters_->inc_submitted();
     const bool elig = eligible(op_id, inputs, output);
+    // fusion (runtime.hpp:270-281): chainable elementwise steps accumulate
+    if (fusion_on_ && elig && scalars.empty() && chainable(op_id, inputs, output)) {
+      if (chain_try_append(op_id, inputs, output, cell, id)) {
+        if (chain_.size() >= std::min<size_t>(cfg_.max_chain, GPUOS_MAX_FUSED + 1)) flush_chain();
+        return h;
+      }
+      flush_chain();
+      if (chain_try_append(op_id, inputs, output, cell, id)) {
+        if (chain_.size() >= std::min<size_t>(cfg_.max_chain, GPUOS_MAX_FUSED + 1)) flush_chain();
+        return h;
+      }
+    }
+    if (!chain_.empty()) flush_chain();  // later work must observe chained writes
     route(op_id, inputs, output, scalars, cell, id, elig, 0);
     return h;
   }
 
-  // ---- fusion (next row of SURVEY §8(f); the chain is not fused yet) ----
-  void set_fusion(bool on) { fusion_on_ = on; }
+  // ---- fusion (runtime.hpp:296-327, 641-933) ----
+  /// Accumulate elementwise chains on submit; turning fusion off flushes.
+  void set_fusion(bool on) {
+    if (!on) flush_chain();
+    fusion_on_ = on;
+  }
   bool fusion() const { return fusion_on_; }
-  void fuse() {}
+  /// Flush the pending chain; a no-op when nothing is chained.
+  void fuse() { flush_chain(); }
+  /// Submit a whole chain and flush it as one unit (intermediates elided
+  /// unless a handle other than the returned one is retained).
   std::vector<TaskHandle> fuse(std::span<const OpCall> calls) {
+    const bool prev_on = fusion_on_;
+    const long prev_base = chain_handle_baseline_;
+    fusion_on_ = true;
+    chain_handle_baseline_ = 1;  // the returned vector holds one reference
     std::vector<TaskHandle> out;
     out.reserve(calls.size());
-    for (const OpCall& c : calls) {
-      out.push_back(submit(c));
-      wait(out.back());  // sequential semantics: each step observes the previous
-    }
+    for (const OpCall& c : calls) out.push_back(submit(c));
+    flush_chain();
+    chain_handle_baseline_ = prev_base;
+    fusion_on_ = prev_on;
     return out;
   }
-  uint64_t fusion_absorbed() const { return 0; }
+  /// Submissions folded into composites; submitted == inline + committed + absorbed.
+  uint64_t fusion_absorbed() const { return fusion_absorbed_; }
 
   // ---- injection ----
   uint64_t inject_operator(const std::string& template_name, std::span<const double> params = {},
@@ -562,8 +633,12 @@ class Runtime {
   ModuleCache& module_cache() { return cache_; }
 
   // ---- completion / introspection ----
-  TaskState wait(const TaskHandle& h) { return h.wait(); }
+  TaskState wait(const TaskHandle& h) {
+    if (!chain_.empty()) flush_chain();  // runtime.hpp:392-395
+    return h.wait();
+  }
   void wait_all() {
+    if (!chain_.empty()) flush_chain();
     const int rc = gpuos_ring_wait_processed(dev_, committed_tasks_);
     if (rc != 0 && rc != static_cast<int>(ErrorCode::RuntimeStopped)) check_abi(rc, "wait_all");
   }
@@ -626,13 +701,14 @@ class Runtime {
   }
   void set_yield_every(uint64_t n) { gpuos_set_yield_every(dev_, n); }
   bool stopped() const { return stopped_; }
-  size_t pending_composites() const { return 0; }
+  size_t pending_composites() const { return chain_.size(); }
   gpuos_dev* device() const { return dev_; }
   const RuntimeConfig& config() const { return cfg_; }
 
   /// Drain, stop the worker kernel, release all buffers; idempotent.
   void shutdown() {
     if (stopped_) return;
+    flush_chain();
     wait_all();
     stopped_ = true;
     gpuos_dev_stop(dev_);
@@ -737,6 +813,235 @@ class Runtime {
       out->addr = reinterpret_cast<uint64_t>(static_cast<char*>(b->data) + v.offset * static_cast<int64_t>(dtype_width(v.dtype)));
     }
     return true;
+  }
+
+  // ---- fusion machinery ----
+  struct ChainStep {
+    uint64_t op_id;
+    std::vector<TensorView> inputs;
+    TensorView output;
+    uint32_t cell;
+    uint64_t id;
+  };
+
+  /// Structural screen (runtime.hpp:643-673).
+  bool chainable(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output) const {
+    if (output.dtype != DType::F32 && output.dtype != DType::F64) return false;
+    for (const TensorView& v : inputs)
+      if (v.dtype != output.dtype) return false;
+    size_t want = 0;
+    if (op_id >= kFirstInjectedId) {
+      const auto it = modules_by_id_.find(static_cast<uint32_t>(op_id));
+      if (it == modules_by_id_.end()) return false;
+      want = static_cast<size_t>(it->second->signature.arity);
+      if (it->second->signature.dtype != output.dtype) return false;
+    } else {
+      switch (static_cast<OpKind>(op_id)) {
+        case OpKind::Add: case OpKind::Mul: want = 2; break;
+        case OpKind::Relu: case OpKind::Gelu: want = 1; break;
+        default: return false;
+      }
+      if (table_->latest_entry(op_id).status != OpStatus::Active) return false;
+    }
+    return inputs.size() == want;
+  }
+
+  /// Aliasing rules of runtime.hpp:678-729.
+  bool chain_try_append(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
+                        uint32_t cell, uint64_t id) {
+    if (!chain_.empty()) {
+      const TensorView& head = chain_.front().output;
+      if (output.dtype != head.dtype || !(output.shape == head.shape)) return false;
+    }
+    size_t fresh = 0;
+    for (const TensorView& in : inputs) {
+      bool inter = false, mismatch = false;
+      for (const ChainStep& st : chain_) {
+        if (in.buffer != st.output.buffer) continue;
+        if (in.same_layout(st.output)) inter = true;
+        else mismatch = true;
+      }
+      if (mismatch && !inter) return false;
+      if (inter) continue;
+      bool known = false;
+      for (const TensorView& e : chain_externals_)
+        if (in.same_layout(e)) known = true;
+      if (!known) ++fresh;
+    }
+    if (chain_externals_.size() + fresh > kMaxInputs) return false;
+    for (const TensorView& e : chain_externals_)
+      if (output.buffer == e.buffer) return false;  // would invalidate a folded read
+    for (const ChainStep& st : chain_)
+      if (output.buffer == st.output.buffer && !output.same_layout(st.output)) return false;
+    for (const TensorView& in : inputs) {
+      bool inter = false, known = false;
+      for (const ChainStep& st : chain_)
+        if (in.same_layout(st.output)) inter = true;
+      if (inter) continue;
+      for (const TensorView& e : chain_externals_)
+        if (in.same_layout(e)) known = true;
+      if (!known) chain_externals_.push_back(in);
+    }
+    chain_.push_back(ChainStep{op_id, std::vector<TensorView>(inputs.begin(), inputs.end()), output, cell, id});
+    return true;
+  }
+
+  /// Builtins re-expressed in the kernels' evaluation order (runtime.hpp:734-762).
+  ExprPtr step_ast(const ChainStep& st) const {
+    if (st.op_id >= kFirstInjectedId) return clone(*modules_by_id_.at(static_cast<uint32_t>(st.op_id))->folded_ast);
+    switch (static_cast<OpKind>(st.op_id)) {
+      case OpKind::Add: return make_binary(ExprKind::Add, make_in(0), make_in(1));
+      case OpKind::Mul: return make_binary(ExprKind::Mul, make_in(0), make_in(1));
+      case OpKind::Relu: return make_binary(ExprKind::Max, make_in(0), make_const(0.0));
+      case OpKind::Gelu: {
+        const double c = std::sqrt(2.0 / 3.14159265358979323846);
+        ExprPtr x3 = make_binary(
+            ExprKind::Mul,
+            make_binary(ExprKind::Mul, make_binary(ExprKind::Mul, make_const(0.044715), make_in(0)), make_in(0)),
+            make_in(0));
+        ExprPtr inner = make_binary(ExprKind::Mul, make_const(c), make_binary(ExprKind::Add, make_in(0), std::move(x3)));
+        ExprPtr outer = make_binary(ExprKind::Add, make_const(1.0), make_unary(ExprKind::Tanh, std::move(inner)));
+        return make_binary(ExprKind::Mul, make_binary(ExprKind::Mul, make_const(0.5), make_in(0)), std::move(outer));
+      }
+      default: throw Error(ErrorCode::Internal, "unfusable op in chain");
+    }
+  }
+
+  bool retained(const ChainStep& st) const { return cells_->use_count(st.cell) > chain_handle_baseline_; }
+
+  void flush_chain() {
+    if (chain_.empty()) return;
+    std::vector<ChainStep> steps = std::move(chain_);
+    chain_.clear();
+    chain_externals_.clear();
+    size_t i = 0;
+    while (i < steps.size()) {
+      size_t j = i;
+      while (j + 1 < steps.size() && !retained(steps[j])) ++j;
+      publish_segment(steps, i, j, /*blocking=*/j + 1 < steps.size());
+      i = j + 1;
+    }
+  }
+
+  void wait_cell(uint32_t cell, uint64_t id) const {
+    for (uint32_t spin = 0;; ++spin) {
+      const uint64_t w = __atomic_load_n(cells_->word(cell), __ATOMIC_ACQUIRE);
+      if ((w & 0xffu) != 0 && (w >> 16) == (id & detail::CellPool::kSeqMask)) return;
+      if (spin > 4096) std::this_thread::yield();
+      else __builtin_ia32_pause();
+    }
+  }
+
+  /// Steps [i..j] as one composite task at the composite id (runtime.hpp:785-908).
+  void publish_segment(std::vector<ChainStep>& steps, size_t i, size_t j, bool blocking) {
+    if (i == j) {  // a single step publishes as itself
+      const ChainStep& st = steps[i];
+      route(st.op_id, st.inputs, st.output, {}, st.cell, st.id, true, 0);
+      if (blocking) wait_cell(st.cell, st.id);
+      return;
+    }
+    const DType dtype = steps[j].output.dtype;
+    std::vector<TensorView> ext;
+    std::vector<std::pair<TensorView, ExprPtr>> inter;  // produced within this segment
+    ExprPtr cur;
+    for (size_t k = i; k <= j; ++k) {
+      const ChainStep& st = steps[k];
+      const ExprPtr base = step_ast(st);
+      cur = rewrite_inputs(*base, [&](int idx) -> ExprPtr {
+        const TensorView& v = st.inputs[static_cast<size_t>(idx)];
+        for (const auto& [iv, ie] : inter)
+          if (v.same_layout(iv)) return clone(*ie);
+        for (size_t e = 0; e < ext.size(); ++e)
+          if (v.same_layout(ext[e])) return make_in(static_cast<int>(e));
+        ext.push_back(v);
+        return make_in(static_cast<int>(ext.size() - 1));
+      });
+      if (k < j) {  // materialization boundary: narrow to the stored dtype
+        ExprPtr narrowed = make_narrow(dtype, clone(*cur));
+        bool replaced = false;
+        for (auto& [iv, ie] : inter)
+          if (iv.same_layout(st.output)) {
+            ie = std::move(narrowed);
+            replaced = true;
+            break;
+          }
+        if (!replaced) inter.emplace_back(st.output, std::move(narrowed));
+      }
+    }
+    auto sequential = [&] {
+      for (size_t k = i; k <= j; ++k) execute_inline(steps[k].op_id, steps[k].inputs, steps[k].output, {}, steps[k].cell, steps[k].id);
+    };
+    if (ext.size() > kMaxInputs) {
+      sequential();
+      return;
+    }
+    OperatorSignature sig;
+    {
+      std::string canon;
+      detail::canonical_expr(*cur, canon);
+      sig.template_name = "fused_" + canon;
+    }
+    sig.dtype = dtype;
+    sig.arity = static_cast<int>(ext.size());
+    const uint64_t h0 = cache_.hits(), m0 = cache_.misses();
+    ModulePtr mod;
+    try {
+      mod = cache_.compile_or_get_ast(sig, [&] { return clone(*cur); });
+    } catch (...) {
+      sync_cache_counters(h0, m0);
+      sequential();  // e.g. deeper than the verifier's stack bound: sequential semantics
+      return;
+    }
+    sync_cache_counters(h0, m0);
+    const std::string key = signature_key(sig);
+    uint64_t prog = 0;
+    if (auto it = composite_programs_.find(key); it != composite_programs_.end()) {
+      prog = it->second;
+    } else {
+      const std::vector<gpuos_instr> img = to_device_program(mod->bytecode);
+      check_abi(gpuos_program_upload(dev_, img.data(), static_cast<uint32_t>(img.size()), sig.arity,
+                                     static_cast<int>(dtype), &prog),
+                "composite program");
+      composite_programs_.emplace(key, prog);
+    }
+    fusion_absorbed_ += j - i;  // j-i+1 steps behind one descriptor
+    const ChainStep& last = steps[j];
+    uint64_t rec_dev = 0;
+    uint64_t* rec = cells_->record(last.cell, &rec_dev);
+    rec[0] = j - i;
+    for (size_t k = i; k < j; ++k) {
+      rec[1 + 2 * (k - i)] = cells_->device_addr(steps[k].cell);
+      rec[2 + 2 * (k - i)] = steps[k].id;
+    }
+    double sc[2];
+    std::memcpy(&sc[0], &prog, 8);
+    std::memcpy(&sc[1], &rec_dev, 8);
+    alignas(64) gpuos_task t;
+    build_task(kCompositeOpId, ext, last.output, std::span<const double>(sc, 2), last.cell, last.id,
+               GPUOS_FLAG_FUSED_COMPOSITE, &t);
+    uint64_t pos = 0;
+    if (gpuos_ring_reserve(dev_, &pos) == 0) {
+      gpuos_ring_publish(dev_, pos, &t);
+      counters_->inc_committed();
+      ++committed_tasks_;
+      if (blocking) wait_cell(last.cell, last.id);
+      return;
+    }
+    // queue full: the composite on the conventional path, completed here
+    counters_->inc_queue_full_fallback();
+    counters_->inc_inline();
+    ErrorCode code = ErrorCode::Ok;
+    int rc = gpuos_launch_task(dev_, &t, inline_stream_);
+    if (rc == 0) rc = gpuos_stream_sync(dev_, inline_stream_);
+    if (rc != 0) {
+      code = static_cast<ErrorCode>(rc);
+    } else {
+      const uint64_t w = __atomic_load_n(cells_->word(last.cell), __ATOMIC_ACQUIRE);
+      code = (w & 0xffu) == 1 ? ErrorCode::Ok : static_cast<ErrorCode>((w >> 8) & 0xffu);
+    }
+    if (code != ErrorCode::Ok) counters_->inc_failed();
+    counters_->inc_op(kCompositeOpId);
+    for (size_t k = i; k <= j; ++k) cells_->complete(steps[k].cell, steps[k].id, code);
   }
 
   bool build_task(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
@@ -918,6 +1223,11 @@ class Runtime {
   std::map<uint32_t, std::string> native_obj_;
   std::unordered_map<std::string, std::string> native_cache_;
   NativeStats last_native_{};
+  std::vector<ChainStep> chain_;
+  std::vector<TensorView> chain_externals_;
+  uint64_t fusion_absorbed_ = 0;
+  long chain_handle_baseline_ = 0;  // a step is retained while more handles than this reference it
+  std::unordered_map<std::string, uint64_t> composite_programs_;  // fused signature -> device program
 
   static std::string native_symbol(const std::string& key) {
     uint64_t h = 1469598103934665603ull;  // FNV-1a of the signature key

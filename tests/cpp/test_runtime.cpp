@@ -581,6 +581,62 @@ TEST_CASE("native promotion: NVRTC + nvJitLink op, generation handover, bit-iden
               compile_ms, link_ms, handover_us);
 }
 
+TEST_CASE("fusion: composites equal the waited sequential run; retained steps materialize") {
+  for (DType dt : {DType::F32, DType::F64}) {
+    Runtime rt(small_config(4096, 0));
+    const double pa[2] = {1.5, -0.25};
+    const uint64_t sa = rt.inject_operator("scale_add", pa, dt);
+    std::mt19937_64 rng(4242);
+    const int64_t n = 4096;
+    auto x = rt.alloc_tensor(dt, {n});
+    auto y = rt.alloc_tensor(dt, {n});
+    fill(rt, x, random_vals(rng, static_cast<size_t>(n), -2.0, 2.0));
+    fill(rt, y, random_vals(rng, static_cast<size_t>(n), -2.0, 2.0));
+    // chain: t1 = x + y; t2 = t1 * x; t3 = relu(t2); t4 = gelu(t3); t5 = scale_add(t4)
+    auto run_chain = [&](bool fused, std::vector<TensorView>& t, bool keep_t2) {
+      for (int k = 0; k < 5; ++k) t.push_back(rt.alloc_tensor(dt, {n}));
+      rt.set_fusion(fused);
+      std::vector<TaskHandle> keep;
+      auto step = [&](uint64_t op, std::vector<TensorView> ins, const TensorView& o, bool hold) {
+        TaskHandle h = rt.submit(op, std::move(ins), o);
+        if (!fused) REQUIRE(rt.wait(h) == TaskState::Done);  // waited sequential
+        if (hold) keep.push_back(h);
+      };
+      step(static_cast<uint64_t>(OpKind::Add), {x, y}, t[0], false);
+      step(static_cast<uint64_t>(OpKind::Mul), {t[0], x}, t[1], keep_t2);
+      step(static_cast<uint64_t>(OpKind::Relu), {t[1]}, t[2], false);
+      step(static_cast<uint64_t>(OpKind::Gelu), {t[2]}, t[3], false);
+      step(sa, {t[3]}, t[4], true);
+      for (const TaskHandle& h : keep) REQUIRE(rt.wait(h) == TaskState::Done);
+      rt.set_fusion(false);
+    };
+    std::vector<TensorView> seq, fus, fus2;
+    run_chain(false, seq, false);
+    const uint64_t absorbed0 = rt.fusion_absorbed();
+    run_chain(true, fus, false);
+    CHECK(rt.fusion_absorbed() - absorbed0 == 4);  // five steps behind one descriptor
+    REQUIRE(read_all(rt, fus[4]) == read_all(rt, seq[4]));
+    // a retained handle splits the chain and materializes its output
+    run_chain(true, fus2, true);
+    REQUIRE(read_all(rt, fus2[1]) == read_all(rt, seq[1]));
+    REQUIRE(read_all(rt, fus2[4]) == read_all(rt, seq[4]));
+    // fuse(calls): every returned handle completes; the chain's tail is exact
+    std::vector<TensorView> t;
+    for (int k = 0; k < 3; ++k) t.push_back(rt.alloc_tensor(dt, {n}));
+    std::vector<OpCall> calls(3);
+    calls[0] = OpCall{static_cast<uint64_t>(OpKind::Add), {x, y}, t[0], {}};
+    calls[1] = OpCall{static_cast<uint64_t>(OpKind::Mul), {t[0], x}, t[1], {}};
+    calls[2] = OpCall{static_cast<uint64_t>(OpKind::Relu), {t[1]}, t[2], {}};
+    const std::vector<TaskHandle> hs = rt.fuse(calls);
+    for (const TaskHandle& h : hs) REQUIRE(rt.wait(h) == TaskState::Done);
+    REQUIRE(read_all(rt, t[2]) == read_all(rt, seq[2]));
+    rt.wait_all();
+    const CounterSnapshot c = rt.counters();
+    CHECK(c.submitted == c.inline_executions + c.committed + rt.fusion_absorbed());  // runtime.hpp:325-327
+    CHECK(rt.canary_hits() == 0);
+  }
+}
+
 TEST_CASE("shutdown drains every committed task") {
   Runtime rt(small_config(1024, 0));
   auto x = rt.alloc_tensor(DType::F32, {256});
