@@ -198,6 +198,14 @@ def run_configs(lib, local: int) -> dict:
         "window_rows_checked": int(out[6]), "rows_not_one_variant": int(out[7]),
         "old_rows_past_window": int(out[8]), "failed_tasks": int(out[9]), "canary_hits": int(out[10]),
         "old_rows": int(out[11]), "new_rows": int(out[12])}
+    lib.gb_config5.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_config5(local, 8, 50_000, 18, out)
+    res["config5_streams_1gpu"] = {
+        "workload": "8 independent config-2 streams (seeds 42..49) x 50,000 mixed micro-ops, one host producer "
+                    "thread and one runtime (ring + persistent generation of 18 CTAs) per stream, all on this GPU "
+                    "(G=1 of the 1/2/4/8 sharding; bench.py --gpus G runs one replica per GPU)",
+        "tasks_per_s": out[0], "alg_GBps": out[1], "roofline_frac": out[1] / peaks["hbm_gbs"],
+        "failed_tasks": int(out[2]), "slowest_stream_ms": out[3]}
     lib.gb_native.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_native(local, 200_000, out)
     res["config4_native_promotion"] = {

@@ -279,6 +279,16 @@ static int dev_write_field(gpuos_dev* d, size_t off, const void* src, size_t n) 
   return GPUOS_OK;
 }
 
+// A resident worker generation occupies its stream's hardware work queue for
+// its whole life; with CUDA's default of 8 queues (CUDA_DEVICE_MAX_CONNECTIONS)
+// several runtimes -- or one runtime plus enough other streams -- can land
+// later work (memsets, copies, per-op launches) behind a persistent kernel
+// and deadlock.  Ask for 32 unless the process already chose; this must run
+// before CUDA initialises, hence a load-time constructor.
+__attribute__((constructor)) static void gpuos_connections_default() {
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+}
+
 extern "C" {
 
 int gpuos_abi_version(void) { return GPUOS_ABI_VERSION; }

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace gpuos;
@@ -558,6 +559,73 @@ int gb_native(int device, int n_tasks, double* out) {
   out[7] = st.handover.relaunch_ns / 1e3;
   out[8] = (st.install.upload_ns + st.install.epoch_wait_ns + st.install.bank_write_ns + st.install.flip_ns) / 1e3;
   out[9] = static_cast<double>(bad);
+  return 0;
+}
+
+// Config 5 on one GPU: `streams` independent task streams (config-2
+// distribution, seeds 42+s), each from its own host producer thread into its
+// own runtime (ring + persistent generation of `workers` CTAs: the streams
+// split the SMs), all on `device`.  On G GPUs the same streams shard s -> s%G
+// (bench.py --gpus G runs one replica per GPU).
+// out: [0] aggregate tasks/s (all streams / slowest stream's device time),
+//      [1] aggregate algorithmic GB/s, [2] failed tasks, [3] slowest stream ms
+int gb_config5(int device, int streams, int tasks_per_stream, int workers, double* out) {
+  struct Stream {
+    std::unique_ptr<Runtime> rt;
+    Mixed m;
+    double ms = 0;
+    uint64_t failed = 0;
+  };
+  std::vector<Stream> ss(static_cast<size_t>(streams));
+  for (int i = 0; i < streams; ++i) {
+    RuntimeConfig cfg = bench_cfg(device, 4096);
+    cfg.workers.num_workers = static_cast<size_t>(workers);
+    ss[static_cast<size_t>(i)].rt = std::make_unique<Runtime>(cfg);
+    ss[static_cast<size_t>(i)].m = make_mixed(*ss[static_cast<size_t>(i)].rt, tasks_per_stream, 42 + static_cast<uint64_t>(i));
+    ss[static_cast<size_t>(i)].rt->wait_all();
+  }
+  auto run = [&](Stream& st) {
+    Runtime& rt = *st.rt;
+    std::vector<TaskHandle> hs;
+    hs.reserve(st.m.calls.size());
+    void *e0 = nullptr, *e1 = nullptr, *ks = nullptr;
+    check_abi(gpuos_event_create(rt.device(), &e0), "ev");
+    check_abi(gpuos_event_create(rt.device(), &e1), "ev");
+    check_abi(gpuos_dev_kernel_stream(rt.device(), &ks), "ks");
+    check_abi(gpuos_dev_stop(rt.device()), "stop");
+    check_abi(gpuos_event_record(rt.device(), e0, ks), "ev0");
+    check_abi(gpuos_dev_start(rt.device()), "start");
+    check_abi(gpuos_event_record(rt.device(), e1, ks), "ev1");
+    for (const Gen& g : st.m.calls)
+      hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), std::span<const TensorView>(g.in), g.out,
+                                  std::span<const double>()));
+    rt.wait_all();
+    check_abi(gpuos_dev_stop(rt.device()), "stop");
+    check_abi(gpuos_event_sync(rt.device(), e1), "sync");
+    float ms = 0;
+    check_abi(gpuos_event_elapsed_ms(rt.device(), e0, e1, &ms), "elapsed");
+    st.ms = ms;
+    for (const TaskHandle& h : hs) st.failed += h.state() == TaskState::Failed ? 1 : 0;
+    gpuos_event_destroy(rt.device(), e0);
+    gpuos_event_destroy(rt.device(), e1);
+    check_abi(gpuos_dev_start(rt.device()), "restart");
+  };
+  for (Stream& st : ss) run(st);  // warm each stream alone
+  std::vector<std::thread> th;
+  for (Stream& st : ss) th.emplace_back([&run, &st] { run(st); });
+  for (std::thread& t : th) t.join();
+  double slow = 0, bytes = 0;
+  uint64_t failed = 0, tasks = 0;
+  for (const Stream& st : ss) {
+    slow = std::max(slow, st.ms);
+    bytes += st.m.bytes;
+    failed += st.failed;
+    tasks += st.m.calls.size();
+  }
+  out[0] = static_cast<double>(tasks) / (slow / 1e3);
+  out[1] = bytes / (slow / 1e3) / 1e9;
+  out[2] = static_cast<double>(failed);
+  out[3] = slow;
   return 0;
 }
 
