@@ -340,6 +340,13 @@ struct RuntimeConfig {
   /// Task buffers in plain device memory instead of managed memory (faster
   /// host<->device copies; host access only through pool().upload/download).
   bool device_buffers = false;
+  /// Backpressure before the queue-full fallback: how long submit keeps
+  /// retrying a full ring before it runs the task inline (runtime.hpp:562-564
+  /// falls back at once).  The inline path here is a kernel launch + sync
+  /// (~15 us), while the workers free a slot every few hundred ns, so a short
+  /// wait is the cheaper way to absorb a producer that outruns the device.
+  /// 0 = the reference's immediate fallback.  Env GPUOS_QUEUE_SPIN_NS.
+  uint64_t queue_full_spin_ns = 50000;
 
   /// GPUOS_CAPACITY, GPUOS_WORKERS, GPUOS_YIELD_EVERY, GPUOS_MAX_ELEMS, GPUOS_DEVICE.
   static RuntimeConfig from_env() {
@@ -349,6 +356,7 @@ struct RuntimeConfig {
     c.workers.yield_every = env_u64("GPUOS_YIELD_EVERY", c.workers.yield_every);
     c.max_elements = env_u64("GPUOS_MAX_ELEMS", c.max_elements);
     c.device = static_cast<int>(env_u64("GPUOS_DEVICE", static_cast<uint64_t>(c.device)));
+    c.queue_full_spin_ns = env_u64("GPUOS_QUEUE_SPIN_NS", c.queue_full_spin_ns);
     return c;
   }
 
@@ -1020,7 +1028,7 @@ class Runtime {
     build_task(kCompositeOpId, ext, last.output, std::span<const double>(sc, 2), last.cell, last.id,
                GPUOS_FLAG_FUSED_COMPOSITE, &t);
     uint64_t pos = 0;
-    if (gpuos_ring_reserve(dev_, &pos) == 0) {
+    if (reserve_with_backpressure(&pos)) {
       gpuos_ring_publish(dev_, pos, &t);
       counters_->inc_committed();
       ++committed_tasks_;
@@ -1108,7 +1116,14 @@ class Runtime {
       t.addr[k] = reinterpret_cast<uint64_t>(static_cast<char*>(b->data) + v.offset * static_cast<int64_t>(w));
     }
     for (size_t k = inputs.size() + 1; k <= GPUOS_MAX_INPUTS; ++k) t.addr[k] = 0;
-    const int rc = gpuos_ring_submit_dense(dev_, &t);
+    int rc = gpuos_ring_submit_dense(dev_, &t);
+    if (rc == static_cast<int>(ErrorCode::QueueFull) && cfg_.queue_full_spin_ns) {
+      const uint64_t t0 = monotonic_ns();
+      do {
+        _mm_pause();
+        rc = gpuos_ring_submit_dense(dev_, &t);
+      } while (rc == static_cast<int>(ErrorCode::QueueFull) && monotonic_ns() - t0 < cfg_.queue_full_spin_ns);
+    }
     *full = rc == static_cast<int>(ErrorCode::QueueFull);
     return rc == 0;
   }
@@ -1134,7 +1149,7 @@ class Runtime {
     alignas(64) gpuos_task t;
     if (elig && op_id <= UINT32_MAX && build_task(op_id, inputs, output, scalars, cell, id, flags, &t)) {
       uint64_t pos = 0;
-      if (gpuos_ring_reserve(dev_, &pos) == 0) {
+      if (reserve_with_backpressure(&pos)) {
         gpuos_ring_publish(dev_, pos, &t);
         counters_->inc_committed();
         ++committed_tasks_;
@@ -1143,6 +1158,17 @@ class Runtime {
       counters_->inc_queue_full_fallback();
     }
     execute_inline(op_id, inputs, output, scalars, cell, id);
+  }
+
+  bool reserve_with_backpressure(uint64_t* pos) {
+    if (gpuos_ring_reserve(dev_, pos) == 0) return true;
+    if (!cfg_.queue_full_spin_ns) return false;
+    const uint64_t t0 = monotonic_ns();
+    do {
+      _mm_pause();
+      if (gpuos_ring_reserve(dev_, pos) == 0) return true;
+    } while (monotonic_ns() - t0 < cfg_.queue_full_spin_ns);
+    return false;
   }
 
   void execute_inline(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,

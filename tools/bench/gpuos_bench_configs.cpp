@@ -40,11 +40,16 @@ uint64_t config_seed(uint64_t seed, uint64_t config) {  // bench.hpp:280-282
   return seed ^ (config * 0x9e3779b97f4a7c15ull + 0x2545f4914f6cdd1dull);
 }
 
-struct Gen {  // one generated call of config 2
+struct Gen {  // one generated call of config 2 (operands inline: the stream is walked once, in order)
   OpKind op;
-  std::vector<TensorView> in;
+  struct In {
+    TensorView v[2];
+    int n = 0;
+    void push_back(TensorView x) { v[n++] = std::move(x); }
+  } in;
   TensorView out;
   double bytes;
+  std::span<const TensorView> inputs() const { return std::span<const TensorView>(in.v, static_cast<size_t>(in.n)); }
 };
 
 TensorView view_of(const TensorView& base, int64_t offset, Shape shape, Strides strides) {
@@ -113,12 +118,24 @@ Mixed make_mixed(Runtime& rt, int n_tasks, uint64_t seed) {
   };
   std::vector<Plan> plans(static_cast<size_t>(n_tasks));
   int64_t out_need[4] = {0, 0, 0, 0};
+  // GB_FORCE_{OP,DT,LAYOUT,SUB} pin one dimension of the distribution
+  // (diagnostics: per-kind device cost)
+  auto forced = [](const char* name) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : -1;
+  };
+  const int f_op = forced("GB_FORCE_OP"), f_dt = forced("GB_FORCE_DT"), f_lay = forced("GB_FORCE_LAYOUT"),
+            f_sub = forced("GB_FORCE_SUB");
   for (Plan& p : plans) {
     p.op = pick4(rng);
     p.dt = pick4(rng);
     p.n = static_cast<int64_t>(std::llround(std::exp(lg(rng))));
     p.layout = pick3(rng);
     p.sub = pick2(rng);
+    if (f_op >= 0) p.op = f_op;
+    if (f_dt >= 0) p.dt = f_dt;
+    if (f_lay >= 0) p.layout = f_lay;
+    if (f_sub >= 0) p.sub = f_sub;
     // a 2-D factorisation R x C ~ n with R a power of two
     int64_t r = 1;
     while (r * r * 4 < p.n) r <<= 1;
@@ -258,7 +275,7 @@ int gb_config2(int device, int n_tasks, int steps, double* out) {
     const double ms = ev.generation([&] {
       const double t0 = now_ms();
       for (const Gen& g : m.calls)
-        hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), std::span<const TensorView>(g.in), g.out, std::span<const double>()));
+        hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), g.inputs(), g.out, std::span<const double>()));
       t_sub = now_ms() - t0;
       rt.wait_all();
     });
@@ -597,8 +614,7 @@ int gb_config5(int device, int streams, int tasks_per_stream, int workers, doubl
     check_abi(gpuos_dev_start(rt.device()), "start");
     check_abi(gpuos_event_record(rt.device(), e1, ks), "ev1");
     for (const Gen& g : st.m.calls)
-      hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), std::span<const TensorView>(g.in), g.out,
-                                  std::span<const double>()));
+      hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), g.inputs(), g.out, std::span<const double>()));
     rt.wait_all();
     check_abi(gpuos_dev_stop(rt.device()), "stop");
     check_abi(gpuos_event_sync(rt.device(), e1), "sync");

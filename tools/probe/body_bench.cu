@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256, 1) body_bench(gpuos_task task, int reps, 
   c.smem_bytes = 0;
   c.aux = 0;
   c.flags = 0;
+  c.tmem = kNoTmem;
   long long best = 1ll << 60, sum = 0;
   for (int r = 0; r < reps; ++r) {
     asm volatile("bar.sync 1, 256;" ::: "memory");
