@@ -162,6 +162,39 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
     }
     return;
   }
+  if (s.rank == 2) {
+    // two coalesced dims (row broadcasts, transposed 2-D views): strides and
+    // the column divisor in registers, one divmod per element
+    int64_t st0[1 + A], st1[1 + A];
+#pragma unroll
+    for (int k = 0; k <= A; ++k) {
+      st0[k] = s.st[k][0];
+      st1[k] = s.st[k][1];
+    }
+    const FastDiv fd = s.fd[1];
+    constexpr int U2 = 8;
+    const int64_t step = (int64_t)c->nthreads * U2;
+    for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
+      double x[U2][A];
+      int64_t oo[U2];
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) {
+          const uint32_t q = fd.div((uint32_t)e), r = (uint32_t)e - q * fd.d;
+          oo[u] = (int64_t)q * st0[0] + (int64_t)r * st1[0];
+#pragma unroll
+          for (int k = 0; k < A; ++k) x[u][k] = DT_<DT>::gload(in[k] + (int64_t)q * st0[1 + k] + (int64_t)r * st1[1 + k]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) DT_<DT>::store(out + oo[u], f(x[u]));
+      }
+    }
+    return;
+  }
   // U elements per thread per round, all loads issued before any use, so a
   // round costs one memory latency instead of U
   constexpr int U = 4;

@@ -313,6 +313,28 @@ __device__ __noinline__ int op_layernorm(const gpuos_task* t, const Ctx* c) {
 }
 
 // ---- reductions over the last axis ----
+// This lane's part of a row sum in fp64: kSumUnroll loads in flight before
+// they are added (the fp64 sum of <= 64K narrower values rounds to the same
+// output as the reference's left-to-right order, SURVEY §8(a) "<= 1 ulp").
+constexpr int kSumUnroll = 8;
+template <int DT>
+__device__ __forceinline__ double lane_sum(const char* ib, int64_t si, int64_t cols, const RowSched& rs) {
+  typedef typename DT_<DT>::T T;
+  const T* p = (const T*)ib;
+  double s = 0.0;
+  for (int64_t j0 = rs.lane; j0 < cols; j0 += (int64_t)rs.width * kSumUnroll) {
+    double v[kSumUnroll];
+#pragma unroll
+    for (int u = 0; u < kSumUnroll; ++u) {
+      const int64_t j = j0 + (int64_t)u * rs.width;
+      v[u] = j < cols ? DT_<DT>::gload(p + j * si) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kSumUnroll; ++u) s += v[u];
+  }
+  return s;
+}
+
 template <int MODE>  // 0 sum, 1 max, 2 min
 __device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
@@ -343,11 +365,25 @@ __device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
       if (dt == GPUOS_I32) {
         // exact integer accumulation == the reference's exact-in-double sum
         long long s = 0;
-        for (int64_t j = rs.lane; j < cols; j += rs.width) s += ((const int32_t*)ib)[j * si];
+        for (int64_t j0 = rs.lane; j0 < cols; j0 += (int64_t)rs.width * kSumUnroll) {
+          int32_t v[kSumUnroll];
+#pragma unroll
+          for (int u = 0; u < kSumUnroll; ++u) {
+            const int64_t j = j0 + (int64_t)u * rs.width;
+            v[u] = j < cols ? __ldcg((const int32_t*)ib + j * si) : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kSumUnroll; ++u) s += v[u];
+        }
         r = (double)(long long)unit_sum((double)s, rs, c, (double*)c->smem);
       } else {
         double s = 0.0;
-        for (int64_t j = rs.lane; j < cols; j += rs.width) s += load_any(dt, ib, j * si);
+        switch (dt) {
+          case GPUOS_F32: s = lane_sum<GPUOS_F32>(ib, si, cols, rs); break;
+          case GPUOS_F64: s = lane_sum<GPUOS_F64>(ib, si, cols, rs); break;
+          case GPUOS_F16: s = lane_sum<GPUOS_F16>(ib, si, cols, rs); break;
+          default: s = lane_sum<GPUOS_BF16>(ib, si, cols, rs); break;
+        }
         r = unit_sum(s, rs, c, (double*)c->smem);
       }
     } else {
