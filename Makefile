@@ -14,7 +14,7 @@ CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -I
 LIBDIR := paper_2604_17861_b200/lib
 CSRC := paper_2604_17861_b200/csrc
 OBJ := build/obj
-DEV_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dev_state.h $(CSRC)/ring_format.h include/gpuos_cuda.h
+DEV_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/dev_state.h include/gpuos_ring_format.h include/gpuos_cuda.h
 HOST_HDRS := $(wildcard paper_2604_17861_b200/include/gpuos/*.hpp) include/gpuos_cuda.h
 
 all: lib bench cpp-tests oracle

@@ -318,6 +318,7 @@ typedef struct gpuos_dense_task {
   double scalar0;
 } gpuos_dense_task;
 int gpuos_ring_submit_dense(gpuos_dev* dev, const gpuos_dense_task* task);
+
 /* Monitoring snapshot; head <= tail always holds. */
 int gpuos_ring_peek(gpuos_dev* dev, gpuos_snapshot* out);
 /* Block until processed >= `count` (wait_all, runtime.hpp:399-406). */

@@ -31,6 +31,12 @@
 
 #include "gpuos_cuda.h"
 
+#ifdef __CUDACC__
+#define GPUOS_RING_FN __host__ __device__ __forceinline__
+#else  // host-only C++ (the runtime header writes dense slots inline)
+#define GPUOS_RING_FN inline
+#endif
+
 namespace gdev {
 
 constexpr uint32_t kRingSlot = 128;  // bytes per ring slot
@@ -41,11 +47,11 @@ constexpr uint32_t kFmtExtended = 0;
 constexpr uint32_t kFmtCompact = 1;
 constexpr uint32_t kExtChecksumSalt = 40;
 
-__host__ __device__ __forceinline__ uint64_t ring_term(uint64_t w, uint32_t i) { return w * (uint64_t)(2 * i + 1); }
+GPUOS_RING_FN uint64_t ring_term(uint64_t w, uint32_t i) { return w * (uint64_t)(2 * i + 1); }
 
 // Row-major contiguous strides of `rank` extents (unit dims included), the
 // strides a compact view expands to.
-__host__ __device__ __forceinline__ void contiguous_strides4(const int32_t* ext, int rank, int32_t* st) {
+GPUOS_RING_FN void contiguous_strides4(const int32_t* ext, int rank, int32_t* st) {
   int64_t s = 1;
   for (int d = 3; d >= 0; --d) {
     if (d >= rank) {

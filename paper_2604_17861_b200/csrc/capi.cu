@@ -29,7 +29,7 @@
 
 #include "dev_common.cuh"
 #include "dev_state.h"
-#include "ring_format.h"
+#include "gpuos_ring_format.h"
 #include "gpuos_cuda.h"
 
 #include <dlfcn.h>
@@ -188,7 +188,6 @@ struct gpuos_dev {
   uint64_t* mir_epoch = nullptr;
   uint64_t cap = 0, mask = 0;
   uint64_t reserve = 0;       // producer cursor (single producer)
-  std::atomic<uint64_t> published{0};
   uint32_t workers = 0, threads = 0, smem = 0;
   std::atomic<bool> running{false};
   uint64_t resume_pos = 0;  // first ticket of the next worker generation
@@ -909,7 +908,6 @@ int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
   dst[7] = h;
   __atomic_store_n(&dst[0], pos + 1, __ATOMIC_RELEASE);
   __atomic_store_n(d->tail, pos + 1, __ATOMIC_RELEASE);
-  d->published.store(pos + 1, std::memory_order_relaxed);
   return GPUOS_OK;
 }
 
@@ -940,7 +938,6 @@ int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
   dst[7] = h;
   __atomic_store_n(&dst[0], p + 1, __ATOMIC_RELEASE);
   __atomic_store_n(d->tail, p + 1, __ATOMIC_RELEASE);
-  d->published.store(p + 1, std::memory_order_relaxed);
   return GPUOS_OK;
 }
 

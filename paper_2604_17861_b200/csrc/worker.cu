@@ -22,7 +22,7 @@
 //     after a gpu-scope release fence, and the per-worker processed count.
 #include "dev_common.cuh"
 #include "dev_state.h"
-#include "ring_format.h"
+#include "gpuos_ring_format.h"
 #include "ops_elementwise.cuh"
 #include "ops_linalg.cuh"
 #include "ops_rowwise.cuh"
