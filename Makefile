@@ -9,7 +9,8 @@ NVCC ?= nvcc
 CXX ?= g++
 CC ?= gcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
+NVEXTRA ?=
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $(NVEXTRA)
 CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -Iinclude -Ipaper_2604_17861_b200/include
 LIBDIR := paper_2604_17861_b200/lib
 CSRC := paper_2604_17861_b200/csrc
@@ -61,8 +62,15 @@ build/cpp/test_host: tests/cpp/test_host.cpp tests/cpp/check.hpp $(HOST_HDRS) $(
 	@mkdir -p build/cpp
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
 
-# GPU-box probes (producer cost breakdown, finite worker generation for ncu)
-probes: build/probe/submit_cost build/probe/profile_worker
+# GPU-box probes (producer cost breakdown, finite worker generation for ncu,
+# task-body call cost, PCIe round-trip floor)
+probes: build/probe/submit_cost build/probe/profile_worker build/probe/body_bench build/probe/pingpong
+build/probe/body_bench: tools/probe/body_bench.cu $(DEV_HDRS)
+	@mkdir -p build/probe
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -I$(CSRC) -o $@ $<
+build/probe/pingpong: tools/probe/pingpong.cu
+	@mkdir -p build/probe
+	$(NVCC) $(ARCH) -O3 -o $@ $<
 build/probe/%: tools/probe/%.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	@mkdir -p build/probe
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread

@@ -1670,7 +1670,7 @@ int gpuos_dev_load_native(gpuos_dev* d, const void* cubin, size_t size, const ui
     return GPUOS_VERIFY_ERROR;
   }
   D.fn_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)d->smem);
-  D.fn_attr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
+  D.fn_attr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, gdev::smem_carveout());
   std::vector<void*> table(gdev::kJitSlots, nullptr);
   for (int i = 0; i < n; ++i) {
     CUdeviceptr gp = 0;

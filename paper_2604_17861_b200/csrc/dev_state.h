@@ -117,6 +117,7 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
 cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st);
 uint32_t worker_smem_bytes();
 uint32_t worker_threads();
+int smem_carveout();  // preferred shared carveout (percent) for every kernel, GPUOS_CARVEOUT overrides
 cudaError_t worker_occupancy(int* per_sm);
 
 #endif  // __CUDACC_RTC__

@@ -15,18 +15,37 @@
 namespace gdev {
 
 // ---- scalar functions in reference evaluation order (no contraction) ----
+// `f32` is the same function on f32 operands without the round trip through
+// double.  It is bit-identical to narrow(op(double(a), double(b))): for + and
+// * a double (53-bit) intermediate rounded to f32 (24-bit) is the correctly
+// rounded f32 result, since 53 >= 2*24 + 2 (double rounding is innocuous),
+// and relu only selects.  No FTZ: nvcc keeps f32 denormals by default.
 struct FAdd {
   static constexpr int A = 2;
+  static constexpr bool kF32 = true;
   __device__ __forceinline__ double operator()(const double* v) const { return __dadd_rn(v[0], v[1]); }
+  __device__ __forceinline__ float f32(const float* v) const { return __fadd_rn(v[0], v[1]); }
 };
 struct FMul {
   static constexpr int A = 2;
+  static constexpr bool kF32 = true;
   __device__ __forceinline__ double operator()(const double* v) const { return __dmul_rn(v[0], v[1]); }
+  __device__ __forceinline__ float f32(const float* v) const { return __fmul_rn(v[0], v[1]); }
 };
 struct FRelu {
   static constexpr int A = 1;
+  static constexpr bool kF32 = true;
   // v < 0 ? 0 : v keeps -0.0 and NaN (ops.hpp:188)
   __device__ __forceinline__ double operator()(const double* v) const { return v[0] < 0.0 ? 0.0 : v[0]; }
+  __device__ __forceinline__ float f32(const float* v) const { return v[0] < 0.0f ? 0.0f : v[0]; }
+};
+template <class F, class = void>
+struct HasF32 {
+  static constexpr bool value = false;
+};
+template <class F>
+struct HasF32<F, decltype((void)F::kF32)> {
+  static constexpr bool value = F::kF32;
 };
 struct FGelu {
   static constexpr int A = 1;
@@ -41,7 +60,10 @@ struct FGelu {
 };
 
 // ---- the shared elementwise driver ----
-template <int DT, class F, int U = 4>
+// kAligned: the caller has checked every operand is 16-byte aligned, so the
+// element-wise (unaligned) loop is not instantiated -- the worker's inline
+// path uses this to stay within its register budget.
+template <int DT, class F, int U = 4, bool kAligned = false>
 __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int64_t n, F f) {
   typedef typename DT_<DT>::T T;
   constexpr int A = F::A;
@@ -54,7 +76,7 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
   for (int k = 0; k < A; ++k) aligned = aligned && (((uintptr_t)in[k] & 15) == 0);
   constexpr int V = 16 / sizeof(T);
   int64_t tail_lo = 0;
-  if (aligned) {
+  if (kAligned || aligned) {
     const int64_t nv = n / V;
     int64_t lo, hi;
     part_range(nv, c->part, c->nparts, 1, &lo, &hi);
@@ -80,10 +102,17 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
           T* eo = reinterpret_cast<T*>(&vo);
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            double x[A];
+            if constexpr (DT == GPUOS_F32 && HasF32<F>::value) {
+              float x[A];
 #pragma unroll
-            for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(ev[k] + j);
-            DT_<DT>::store(eo + j, f(x));
+              for (int k = 0; k < A; ++k) x[k] = reinterpret_cast<const float*>(ev[k])[j];
+              reinterpret_cast<float*>(eo)[j] = f.f32(x);
+            } else {
+              double x[A];
+#pragma unroll
+              for (int k = 0; k < A; ++k) x[k] = DT_<DT>::load(ev[k] + j);
+              DT_<DT>::store(eo + j, f(x));
+            }
           }
           reinterpret_cast<uint4*>(out)[i] = vo;
         }
@@ -91,7 +120,7 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
     }
     if (c->part != c->nparts - 1) return;  // the last partition owns the scalar tail
     tail_lo = nv * V;
-  } else {
+  } else if constexpr (!kAligned) {
     // an operand is not 16-byte aligned (views at arbitrary element offsets):
     // element loads, still coalesced across the warp, with UE elements per
     // thread in flight so a round costs one memory latency, not UE

@@ -20,6 +20,9 @@
 //   * the executor group calls the body through the device jump table; the
 //     completer warp posts the completion word with a system-scope store
 //     after a gpu-scope release fence, and the per-worker processed count.
+#ifdef GPUOS_LAT_STAMPS
+#include <cstdio>
+#endif
 #include "dev_common.cuh"
 #include "dev_state.h"
 #include "gpuos_ring_format.h"
@@ -66,6 +69,8 @@ struct SharedCtl {
   int32_t code;
   uint32_t exit;
   uint32_t plan;  // kPlanDenseSame etc. (dev_common.cuh)
+  uint16_t part, nparts;  // this buffer's share of its task (both groups run one task when idle)
+  uint32_t partial;       // 1: not the task's last part -- the completer posts nothing
   uint32_t pad;
 };
 
@@ -83,6 +88,15 @@ static_assert(sizeof(SharedCtl) <= kCtlStride, "SharedCtl must fit its stride");
 constexpr int kGroups = 2;
 constexpr int kGroupThreads = 128;
 constexpr int kWorkerThreads = 32 + kGroups * kGroupThreads + 32;
+constexpr int kWorkerRegs = 112;  // __maxnreg__ below; the inline dense path spills at 96
+// The resident worker and one standalone task kernel (8 warps x <=80
+// registers) must fit together (the inline fallback runs while the worker is
+// resident).  Warps are dealt round-robin to the four SM sub-partitions, each
+// with a quarter of the register file, so the bound is per sub-partition: the
+// one holding three worker warps and two task-kernel warps.  (At 128 registers
+// the task kernel could not co-reside and the inline fallback deadlocked.)
+static_assert(((kWorkerThreads / 32 + 3) / 4) * kWorkerRegs * 32 + 2 * 80 * 32 <= 65536 / 4,
+              "worker + task kernel exceed a sub-partition's register file");
 constexpr int kCompleterWarp = 1 + kGroups * kGroupThreads / 32;
 constexpr int kBufs = 4;
 // Named barriers: 0 = whole CTA, 1+g = executor group g (task bodies),
@@ -92,6 +106,7 @@ constexpr int kBufs = 4;
 constexpr int kBarFull = 3, kBarDone = 7, kBarEmpty = 11;
 constexpr int kFullCount = 32 + kGroupThreads, kDoneCount = kGroupThreads + 32, kEmptyCount = 64;
 constexpr int kMaxBatch = 4;  // tickets claimed per atomic / slots per warp-wide read
+constexpr uint64_t kSplitMin = 2048;  // output elements below which an idle split is not worth it
 constexpr uint32_t kTmemCols = 256;  // 128 per executor group; the rest stays free for standalone kernels
 constexpr int kBarExecExit = 15;  // both executor groups, before TMEM is released
 // Per-CTA cache of resolved table entries, tagged with the version they were
@@ -121,8 +136,17 @@ struct WorkerHeader {
   uint32_t tmem_base;                   // kTmemCols columns, kTmemCols/kGroups per group
   uint32_t pad_;
   CachedEntry cache[kEntryCache];
+#ifdef GPUOS_LAT_STAMPS
+  long long dbg[16];  // latency bisection (debug builds only)
+#endif
 };
 static_assert(sizeof(WorkerHeader) <= kHeaderBytes, "worker header overflows");
+
+#ifdef GPUOS_LAT_STAMPS
+#define LAT_STAMP(i) (H->dbg[i] = clock64())
+#else
+#define LAT_STAMP(i) ((void)0)
+#endif
 
 // Barrier ids must be immediates where possible (a register id makes ptxas
 // reserve all 16); the per-buffer families dispatch over constants.
@@ -355,7 +379,10 @@ __device__ __forceinline__ void fetcher_exit(const WConst& K, uint32_t w, Worker
                                              bool first_marker_staged) {
   for (int g = first_marker_staged ? 1 : 0; g < kGroups; ++g) {
     const int b = next_buffer(F);
-    if (lane == 0) H->ctl[b].exit = 1;
+    if (lane == 0) {
+      H->ctl[b].exit = 1;
+      H->ctl[b].partial = 0;
+    }
     __syncwarp();
     buf_arrive<kBarFull, kFullCount>(b);
     ++F.k;
@@ -465,6 +492,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
         if (ready == 0 && tb != 0 && lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
         if (ready > 0) {
           const uint64_t t_seen = globaltimer();
+          if (lane == 0) LAT_STAMP(0);
           // No acquire fence: executors read task operands with L2 loads only
           // (coherence rule, dev_common.cuh), issued after this read returned
           // (GPUs do not speculate loads past the validation branch).  An
@@ -485,12 +513,14 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             const bool compact = (raw[6] & 0xff) == kFmtCompact;
             if (compact) {
               expand_compact(raw, task, lane);
+
             } else {
               if (lane < 8) reinterpret_cast<uint4*>(task)[lane] = reinterpret_cast<const uint4*>(raw)[lane];
               __syncwarp();
               fetch_ext(S, K, spos, task, lane);
             }
             __syncwarp();
+            if (lane == 0) LAT_STAMP(1);
             const uint32_t plan = compact ? kPlanDenseSame : plan_task_warp(task, lane);
             bool shutdown = false;
             if (lane == 0) {
@@ -505,6 +535,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
               ctl->yield_every = ye;
               ctl->trace_on = tr;
               ctl->plan = plan;
+              LAT_STAMP(2);
               if (task->flags & GPUOS_FLAG_SHUTDOWN) {
                 atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)spos);
                 quiesce(K, w);
@@ -522,14 +553,42 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
                   ctl->aux = (uint64_t)__double_as_longlong(task->scalars[0]);
                 }
                 ctl->version = ver;
+                LAT_STAMP(3);
                 ctl->t_deq = globaltimer();
               }
             }
             shutdown = __shfl_sync(0xffffffffu, shutdown, 0);
+            // Idle split: with nothing else published, a task large enough to
+            // split runs on both executor groups -- this buffer takes part 0
+            // and the next buffer (the other group's) a copy as part 1.  The
+            // completer retires buffers in order, so the task completes once,
+            // after both halves.
+            const bool split = !shutdown && ready == 1 && nb == 1 && hint_seen <= spos + 1 &&
+                               task->size >= kSplitMin;
+            if (lane == 0) {
+              ctl->part = 0;
+              ctl->nparts = split ? 2 : 1;
+              ctl->partial = split ? 1u : 0u;
+            }
             __syncwarp();
+            if (lane == 0) LAT_STAMP(4);
             buf_arrive<kBarFull, kFullCount>(b);
             ++F.k;
             ++j;
+            if (split) {
+              const int b2 = next_buffer(F);
+              if (lane < 24) reinterpret_cast<uint4*>(&H->task[b2])[lane] = reinterpret_cast<const uint4*>(task)[lane];
+              if (lane < (int)(sizeof(SharedCtl) / 8))
+                reinterpret_cast<uint64_t*>(&H->ctl[b2])[lane] = reinterpret_cast<const uint64_t*>(ctl)[lane];
+              __syncwarp();
+              if (lane == 0) {
+                H->ctl[b2].part = 1;
+                H->ctl[b2].partial = 0;
+              }
+              __syncwarp();
+              buf_arrive<kBarFull, kFullCount>(b2);
+              ++F.k;
+            }
             if (shutdown) {
               // the sentinel's buffer carried the first exit marker
               fetcher_exit(K, w, H, F, lane, true);
@@ -564,7 +623,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
 // completion word is posted to host memory.
 __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHeader* H, const gpuos_task* task,
                                               const SharedCtl* ctl, int code, uint64_t t_end, uint64_t& executed) {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("fence.release.gpu;" ::: "memory");
   if (task->done_cell) {
     const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
     st_relaxed_sys((uint64_t*)task->done_cell, word);
@@ -608,8 +667,36 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHea
   if (ye > 0 && executed % ye == 0) __nanosleep(1000);  // yield_every (executor.hpp:190-193)
 }
 
+// Guarded devirtualisation of the table's hottest entries.  After resolve()
+// has mapped op_id -> kind through the dual-bank table (versioned, aliasable),
+// a builtin add or mul over planned dense f32 operands runs inline instead
+// of through the function pointer: the indirect call saves and restores ~40
+// callee-saved registers through local memory, measured at +2300 cycles on a
+// 64-element task (tools/probe/body_bench.cu).  Any other kind, dtype, layout
+// arity or alignment takes the jump table.  Returns false when it did not run the task.
+struct FAddOrMul {  // one loop for both binary ops (one instantiation, one register budget)
+  static constexpr int A = 2;
+  static constexpr bool kF32 = true;
+  bool mul;
+  __device__ __forceinline__ double operator()(const double* v) const {
+    return mul ? __dmul_rn(v[0], v[1]) : __dadd_rn(v[0], v[1]);
+  }
+  __device__ __forceinline__ float f32(const float* v) const { return mul ? __fmul_rn(v[0], v[1]) : __fadd_rn(v[0], v[1]); }
+};
+__device__ __forceinline__ bool dense_f32_inline(uint32_t kind, const gpuos_task* t, const Ctx* c) {
+  if (kind > GPUOS_OP_MUL || !(c->flags & kPlanDenseSame) || t->views[0].dtype != GPUOS_F32 || t->n_inputs != 2)
+    return false;
+  const int64_t n = numel(t->views[0]);
+  if (n <= 0 || n >= ((int64_t)1 << 31)) return false;
+  if ((t->views[0].addr | t->views[1].addr | t->views[2].addr) & 15) return false;
+  FAddOrMul f;
+  f.mul = kind == GPUOS_OP_MUL;
+  ew_dense<GPUOS_F32, FAddOrMul, 4, true>(t, c, n, f);
+  return true;
+}
+
 // One persistent generation.
-extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_kernel(DevState* S) {
+extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState* S) {
   extern __shared__ __align__(128) char smem[];
   WorkerHeader* H = reinterpret_cast<WorkerHeader*>(smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -651,7 +738,21 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
         if (++exits == kGroups) return;
         continue;
       }
-      if (lane == 0) complete_task(S, w, H, &H->task[b], ctl, ctl->code, ctl->t_end, executed);
+#ifdef GPUOS_LAT_STAMPS
+      if (lane == 0) LAT_STAMP(9);
+#endif
+      if (lane == 0 && !ctl->partial) complete_task(S, w, H, &H->task[b], ctl, ctl->code, ctl->t_end, executed);
+#ifdef GPUOS_LAT_STAMPS
+      if (lane == 0 && !ctl->partial) {
+        LAT_STAMP(10);
+        if (ctl->pos > 40 && ctl->pos % 37 == 0) {
+          const long long* d = H->dbg;
+          printf("LAT pos %llu size %lld part %d/%d: expand %lld plan+ctl %lld resolve %lld arrive %lld | wake %lld fnload %lld body %lld gsync %lld | done-wake %lld complete %lld\n",
+                 (unsigned long long)ctl->pos, (long long)H->task[b].size, ctl->part, ctl->nparts, d[1] - d[0], d[2] - d[1], d[3] - d[2],
+                 d[4] - d[3], d[5] - d[4], d[6] - d[5], d[7] - d[6], d[8] - d[7], d[9] - d[8], d[10] - d[9]);
+        }
+      }
+#endif
       __syncwarp();
       buf_arrive<kBarEmpty, kEmptyCount>(b);
     }
@@ -690,23 +791,43 @@ extern "C" __global__ void __launch_bounds__(kWorkerThreads, 2) gpuos_worker_ker
       return;
     }
     const uint64_t t_wake = globaltimer();
+    if (ctx.tid == 0) LAT_STAMP(5);
     int code = ctl->code;
     if (code == GPUOS_OK) {
+      // Rewrite the whole context each task: the body reads it through a
+      // pointer to local memory, and lines written long ago have left L1
+      // (measured: a field stored at kernel start reloads from L2 at ~330
+      // cycles, a field stored this task at ~50).
+      ctx.tid = tid - 32 - g * kGroupThreads;
+      ctx.nthreads = kGroupThreads;
+      ctx.bar_id = 1 + g;
+      ctx.smem = smem + kHeaderBytes + g * scratch;
+      ctx.smem_bytes = scratch;
+      ctx.tmem = H->tmem_base + (uint32_t)(g * (kTmemCols / kGroups));
+      ctx.mbar = &H->mbar[g];
+      ctx.mma_phase = &H->mma_phase[g];
       ctx.aux = ctl->aux;
       ctx.flags = task->flags | ctl->plan;
+      ctx.part = ctl->part;
+      ctx.nparts = ctl->nparts;
       const uint32_t kind = ctl->kind;
-      OpFn fn;
-      if (kind < kNumKinds) {
-        fn = g_kind_fns[kind];
-      } else {
-        // native injected op, or its device program when this generation's
-        // module does not carry the native code
-        OpFn_ p = jit_fns ? jit_fns[kind - kJitKindBase] : nullptr;
-        fn = p ? reinterpret_cast<OpFn>(p) : op_program;
+      if (ctx.tid == 0) LAT_STAMP(6);
+      if (!dense_f32_inline(kind, task, &ctx)) {
+        OpFn fn;
+        if (kind < kNumKinds) {
+          fn = g_kind_fns[kind];
+        } else {
+          // native injected op, or its device program when this generation's
+          // module does not carry the native code
+          OpFn_ p = jit_fns ? jit_fns[kind - kJitKindBase] : nullptr;
+          fn = p ? reinterpret_cast<OpFn>(p) : op_program;
+        }
+        code = fn(task, &ctx);
       }
-      code = fn(task, &ctx);
+      if (ctx.tid == 0) LAT_STAMP(7);
     }
     group_sync(&ctx);
+    if (ctx.tid == 0) LAT_STAMP(8);
     if (ctx.tid == 0) {
       ctl->code = code;
       ctl->t_fenced = t_wake;
@@ -843,6 +964,10 @@ uint32_t worker_smem_bytes() { return kHeaderBytes + kScratchBytes; }
 // standalone task kernels: descriptor + control block + 64 KB scratch
 uint32_t task_smem_bytes() { return kTaskBytes + kCtlBytes + 64 * 1024; }
 uint32_t worker_threads() { return kWorkerThreads; }
+int smem_carveout() {
+  const char* e = std::getenv("GPUOS_CARVEOUT");
+  return e ? std::atoi(e) : (int)cudaSharedmemCarveoutMaxShared;
+}
 
 // Lazy module loading blocks while the persistent kernel is resident
 // (measured: profiles/r01_probe2_lazy.log), so every kernel is loaded and
@@ -852,8 +977,7 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
   cudaFuncSetAttribute(gpuos_worker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // every kernel asks for the largest shared carveout, so an SM configured by
   // the resident worker also has room for a standalone task kernel
-  cudaFuncSetAttribute(gpuos_worker_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(gpuos_worker_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, gpuos_worker_kernel);
   if (worker_regs) *worker_regs = fa.numRegs;
@@ -862,7 +986,7 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
   for (uint32_t k : kinds) {
     TaskKernel f = task_kernel_for(k);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, task_smem_bytes());
-    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
     cudaFuncGetAttributes(&fa, f);
   }
   cudaFuncGetAttributes(&fa, gpuos_clock_probe);

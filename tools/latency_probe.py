@@ -30,7 +30,7 @@ def summarize(name, ph, t_host=None):
         print(f"  host submit->wait p50 {np.percentile(t_host, 50):.2f} us p99 {np.percentile(t_host, 99):.2f} us")
 
 
-n = 4096
+n = int(os.environ.get("LP_N", "4096"))
 with abi.Device(0, telemetry=True, num_workers=int(os.environ.get("LP_WORKERS", "0"))) as d:
     a, b, c = d.alloc(abi.F32, n), d.alloc(abi.F32, n), d.alloc(abi.F32, n)
     a.write(np.ones(n, np.float32))
@@ -38,7 +38,7 @@ with abi.Device(0, telemetry=True, num_workers=int(os.environ.get("LP_WORKERS", 
     va, vb, vc = (d.view(x.id, abi.F32, [n]) for x in (a, b, c))
     lat = []
     for i in range(300):
-        t = d.make_task(abi.OP["add"], vc, [va, vb])
+        t = d.make_task(int(os.environ.get("LP_OP", abi.OP["add"])), vc, [va, vb])
         t0 = time.perf_counter()
         d.submit(t)
         d.wait_cell(t)

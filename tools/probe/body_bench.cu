@@ -14,7 +14,7 @@ __device__ OpFn g_bench_fns[3] = {op_add, op_relu, op_nop};
 }
 using namespace gdev;
 
-__global__ void __launch_bounds__(256, 1) body_bench(gpuos_task task, int reps, int mode, long long* cyc) {
+__global__ void __launch_bounds__(256, 1) body_bench(gpuos_task task, int reps, int mode, long long* cyc, int idle_ns) {
   __shared__ gpuos_task t;
   if (threadIdx.x == 0) t = task;
   __syncthreads();
@@ -31,6 +31,11 @@ __global__ void __launch_bounds__(256, 1) body_bench(gpuos_task task, int reps, 
   c.tmem = kNoTmem;
   long long best = 1ll << 60, sum = 0;
   for (int r = 0; r < reps; ++r) {
+    if (idle_ns) {
+      // an idle gap like queue depth 1 (the host round trip between tasks)
+      const unsigned long long g0 = globaltimer();
+      while (globaltimer() - g0 < (unsigned long long)idle_ns) __nanosleep(1000);
+    }
     asm volatile("bar.sync 1, 256;" ::: "memory");
     const long long t0 = clock64();
     if (mode == 0) {
@@ -83,10 +88,11 @@ int main() {
       t.views[v].dtype = GPUOS_F32;
     }
     cudaDeviceSetLimit(cudaLimitStackSize, 4096);
+    for (int idle : {0, 10000})
     for (int mode = 0; mode < 5; ++mode) {
-      body_bench<<<1, 256>>>(t, 50, mode, cyc);
+      body_bench<<<1, 256>>>(t, 50, mode, cyc, idle);
       cudaError_t e = cudaDeviceSynchronize();
-      std::printf("n=%6d %-22s best %7lld cycles  mean %7lld cycles (%s)\n", n,
+      std::printf("n=%6d idle=%5dns %-22s best %7lld cycles  mean %7lld cycles (%s)\n", n, idle,
                   mode == 0 ? "jump-table op_add" : mode == 1 ? "inline ew_dense<f32>" : mode == 2 ? "jump-table nop" : mode == 3 ? "inline ew_body<add>" : "jump-table op_add plan", cyc[0], cyc[1], cudaGetErrorString(e));
     }
   }
