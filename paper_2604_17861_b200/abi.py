@@ -320,8 +320,7 @@ class Device:
             idx = self._next_cell % self.ncells
             self._next_cell += 1
             self.cells[idx] = 0
-            t.done_cell = self.cells_dev + 8 * idx
-            t.aux = idx  # host-side bookkeeping only
+            t.done_cell = self.cells_dev + 8 * idx  # aux stays 0: the task keeps the compact slot format
         return t
 
     def submit(self, t: Task) -> int:
@@ -338,7 +337,7 @@ class Device:
 
     def wait_cell(self, t: Task, timeout: float = 10.0) -> int:
         """Block until the task's completion cell is terminal; returns its ErrorCode."""
-        idx = t.aux
+        idx = (t.done_cell - self.cells_dev) // 8
         t0 = time.time()
         while True:
             w = int(self.cells[idx])
