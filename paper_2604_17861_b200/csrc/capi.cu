@@ -544,10 +544,12 @@ int gpuos_dev_start(gpuos_dev* d) {
   s.claim = next;
   s.hint = next;
   s.stop_pos = gdev::kRunning;
-  int rc = dev_write_field(d, offsetof(DevState, claim), &s.claim, 8);
-  if (!rc) rc = dev_write_field(d, offsetof(DevState, hint), &s.hint, 8);
-  if (!rc) rc = dev_write_field(d, offsetof(DevState, stop_pos), &s.stop_pos, 8);
-  if (rc) return rc;
+  // stream-ordered on the kernel stream, ahead of the launch: no host round
+  // trips between the caller's start and the generation (the source is the
+  // persistent shadow, so the async copies may still be in flight here)
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, claim), &s.claim, 8, cudaMemcpyHostToDevice, d->ks));
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, hint), &s.hint, 8, cudaMemcpyHostToDevice, d->ks));
+  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, stop_pos), &s.stop_pos, 8, cudaMemcpyHostToDevice, d->ks));
   return launch_workers(d);
 }
 

@@ -132,6 +132,11 @@ int gb_step(void* h, int mode, double* out) {
     if (mode == 0) {
       for (int i = 0; i < b->n; ++i) rt.submit(OpKind::Add, {b->a[i], b->b[i]}, b->c[i]);
       out[5] = now_ms() - t0;  // producer-side cost of the N submits
+      // the shutdown sentinel goes right behind the batch: the generation
+      // drains every committed task, then exits (ev1), so the device-timed
+      // step ends when the last task completes, not when the host's
+      // wait_all poll notices it
+      check_abi(gpuos_dev_stop(b->dev), "stop");
       rt.wait_all();
     } else {
       // e2e: a three-stage pipeline over chunks of tasks -- H2D of chunk k+1
@@ -190,7 +195,7 @@ int gb_step(void* h, int mode, double* out) {
         if (e) gpuos_event_destroy(b->dev, e);
     }
     const double t1 = now_ms();
-    check_abi(gpuos_dev_stop(b->dev), "stop");
+    if (mode != 0) check_abi(gpuos_dev_stop(b->dev), "stop");
     if (std::getenv("GPUOS_BENCH_TRACE")) {
       std::vector<gpuos_trace_phase> ph(static_cast<size_t>(b->n));
       uint64_t n = 0;
