@@ -144,6 +144,9 @@ class CellPool {
         if ((w & 0xffu) == 0 || (w >> 16) != (prev & kSeqMask)) continue;  // previous task in flight
       }
       b.last_seq[i] = seq;
+      // the caller's handle adopts this first reference: a plain store, since
+      // no handle can name a cell whose count is zero (one RMW saved per task)
+      b.refs[i].store(1, std::memory_order_relaxed);
       return g;
     }
     cursor_ = static_cast<uint32_t>(blocks_.size()) * kBlock;
@@ -151,6 +154,7 @@ class CellPool {
     const uint32_t g = cursor_;
     cursor_ = (cursor_ + 1) % (static_cast<uint32_t>(blocks_.size()) * kBlock);
     blocks_[g >> kBlockBits].last_seq[g & (kBlock - 1)] = seq;
+    blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].store(1, std::memory_order_relaxed);
     return g;
   }
   static constexpr uint64_t kSeqMask = (uint64_t{1} << 48) - 1;
@@ -286,7 +290,8 @@ class TaskHandle {
 
  private:
   friend class Runtime;
-  TaskHandle(detail::CellPool* p, uint32_t cell, uint64_t id) : pool_(p), cell_(cell), id_(id) { ref(); }
+  // adopts the reference CellPool::acquire stored for it
+  TaskHandle(detail::CellPool* p, uint32_t cell, uint64_t id) : pool_(p), cell_(cell), id_(id) {}
   void check() const {
     if (!pool_) throw Error(ErrorCode::Internal, "operation on an invalid task handle");
   }

@@ -103,6 +103,7 @@ int main() {
       for (int i = 0; i < n; ++i) cells[i] = rt.cells_->acquire(rt.next_id_++);
       t1 = now_ns();
       double t_acq = (t1 - t0) / n;
+      for (int i = 0; i < n; ++i) rt.cells_->release(cells[i]);  // the handle-less acquires' references
       volatile int sinkv = 0;
       t0 = now_ns();
       for (int i = 0; i < n; ++i) {
