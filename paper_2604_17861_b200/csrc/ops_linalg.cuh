@@ -24,6 +24,58 @@ __device__ __forceinline__ double mac(double acc, double a, double b, bool exact
 // ---- matmul: a (m,k) x b (k,n) -> out (m,n) ----
 constexpr int kTM = 64, kTN = 64, kTK = 32;
 
+// Staging of one k-step for the 4x4-per-thread grid (TM = nthreads/4 rows):
+// every thread issues its loads back to back into registers (raw element
+// type, 8 per batch), then converts and writes shared memory, so a k-step
+// costs one memory latency per batch instead of one per element.  Same
+// values, same order of accumulation: results are unchanged.
+struct MatStage {
+  const char* ap;
+  const char* bp;
+  int64_t sa0, sa1, sb0, sb1;
+  int m, n, k, i0, j0, k0;
+  double* As;
+  double* Bs;
+};
+template <int DT>
+__device__ __forceinline__ void stage_grid(const MatStage& s, const Ctx* c) {
+  typedef typename DT_<DT>::T T;
+  constexpr int kBatch = 8;
+  const T* A = reinterpret_cast<const T*>(s.ap);
+  const T* B = reinterpret_cast<const T*>(s.bp);
+  const int nt = c->nthreads, tid = c->tid;
+  // A: TM x kTK = 8 * nt elements, exactly one batch per thread
+  {
+    T v[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const int e = tid + nt * q;
+      const int gi = s.i0 + e / kTK, gk = s.k0 + e % kTK;
+      v[q] = (gi < s.m && gk < s.k) ? __ldcg(A + gi * s.sa0 + gk * s.sa1) : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const int e = tid + nt * q;
+      s.As[(e / kTK) * (kTK + 1) + e % kTK] = DT_<DT>::load(&v[q]);
+    }
+  }
+  // B: kTK x kTN = 2048 elements, 2048 / nt / 8 batches per thread
+  for (int b0 = 0; b0 < kTK * kTN; b0 += nt * kBatch) {
+    T v[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const int e = b0 + tid + nt * q;
+      const int gk = s.k0 + e / kTN, gj = s.j0 + e % kTN;
+      v[q] = (e < kTK * kTN && gk < s.k && gj < s.n) ? __ldcg(B + gk * s.sb0 + gj * s.sb1) : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      const int e = b0 + tid + nt * q;
+      if (e < kTK * kTN) s.Bs[(e / kTN) * (kTN + 1) + e % kTN] = DT_<DT>::load(&v[q]);
+    }
+  }
+}
+
 __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 2) return GPUOS_ARITY_ERROR;
   const gpuos_view& out = t->views[0];
@@ -72,15 +124,27 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
     for (int k0 = 0; k0 < k; k0 += kTK) {
-      for (int e = c->tid; e < TM * kTK; e += nt) {
-        const int i = e / kTK, kk = e % kTK;
-        const int gi = i0 + i, gk = k0 + kk;
-        As[i * (kTK + 1) + kk] = (gi < m && gk < k) ? load_any(dt, ap, gi * sa0 + gk * sa1) : 0.0;
+      bool staged = false;
+      if (grid) {
+        const MatStage st{ap, bp, sa0, sa1, sb0, sb1, m, n, k, i0, j0, k0, As, Bs};
+        switch (dt) {
+          case GPUOS_F32: stage_grid<GPUOS_F32>(st, c); staged = true; break;
+          case GPUOS_F64: stage_grid<GPUOS_F64>(st, c); staged = true; break;
+          case GPUOS_I32: stage_grid<GPUOS_I32>(st, c); staged = true; break;
+          default: break;
+        }
       }
-      for (int e = c->tid; e < kTK * kTN; e += nt) {
-        const int kk = e / kTN, j = e % kTN;
-        const int gk = k0 + kk, gj = j0 + j;
-        Bs[kk * (kTN + 1) + j] = (gk < k && gj < n) ? load_any(dt, bp, gk * sb0 + gj * sb1) : 0.0;
+      if (!staged) {
+        for (int e = c->tid; e < TM * kTK; e += nt) {
+          const int i = e / kTK, kk = e % kTK;
+          const int gi = i0 + i, gk = k0 + kk;
+          As[i * (kTK + 1) + kk] = (gi < m && gk < k) ? load_any(dt, ap, gi * sa0 + gk * sa1) : 0.0;
+        }
+        for (int e = c->tid; e < kTK * kTN; e += nt) {
+          const int kk = e / kTN, j = e % kTN;
+          const int gk = k0 + kk, gj = j0 + j;
+          Bs[kk * (kTN + 1) + j] = (gk < k && gj < n) ? load_any(dt, bp, gk * sb0 + gj * sb1) : 0.0;
+        }
       }
       group_sync(c);
       const int kmax = (k - k0) < kTK ? (k - k0) : kTK;
