@@ -29,6 +29,31 @@ constexpr int kTM = 64, kTN = 64, kTK = 32;
 // type, 8 per batch), then converts and writes shared memory, so a k-step
 // costs one memory latency per batch instead of one per element.  Same
 // values, same order of accumulation: results are unchanged.
+// One k-step of the 4x4 register tile.  The fma/mul-add choice is a template
+// parameter so the loop carries one form, and the tiles are read through
+// shared-window addresses: with a runtime select and 64-bit generic
+// pointers, ptxas spilled half of the 16 accumulators inside this loop.
+template <bool kExact>
+__device__ __forceinline__ void mm_kloop(double (&acc)[4][4], const double* As, const double* Bs, int ty, int tx, int R,
+                                         int kmax) {
+  const uint32_t as = (uint32_t)__cvta_generic_to_shared(As) + (uint32_t)(ty * (kTK + 1)) * 8u;
+  const uint32_t bs = (uint32_t)__cvta_generic_to_shared(Bs) + (uint32_t)tx * 8u;
+  const uint32_t astep = (uint32_t)(R * (kTK + 1)) * 8u;
+  for (int kk = 0; kk < kmax; ++kk) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(av[r]) : "r"(as + r * astep + (uint32_t)kk * 8u));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(bv[q]) : "r"(bs + (uint32_t)(kk * (kTN + 1) + 16 * q) * 8u));
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = mac(acc[r][q], av[r], bv[q], kExact);
+  }
+}
+
 struct MatStage {
   const char* ap;
   const char* bp;
@@ -149,17 +174,8 @@ __device__ __noinline__ int op_matmul(const gpuos_task* t, const Ctx* c) {
       group_sync(c);
       const int kmax = (k - k0) < kTK ? (k - k0) : kTK;
       if (grid) {
-        for (int kk = 0; kk < kmax; ++kk) {
-          double av[4], bv[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) av[r] = As[(ty + R * r) * (kTK + 1) + kk];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) bv[q] = Bs[kk * (kTN + 1) + tx + 16 * q];
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[r][q] = mac(acc[r][q], av[r], bv[q], exact);
-        }
+        if (exact) mm_kloop<true>(acc, As, Bs, ty, tx, R, kmax);
+        else mm_kloop<false>(acc, As, Bs, ty, tx, R, kmax);
       } else {
         // each thread owns tile elements e = tid + nt*s (s < 16)
         for (int s = 0; s < 16; ++s) {

@@ -53,12 +53,13 @@ int main(int argc, char** argv) {
   // PW_OP=matmul_bf16: n bf16 matmul tasks (128x64 . 64x128, K as a
   // transposed view) for tensor-pipe evidence instead of config-1 adds
   const char* pw = std::getenv("PW_OP");
-  if (pw && std::string(pw) == "matmul_bf16") {
+  if (pw && (std::string(pw) == "matmul_bf16" || std::string(pw) == "matmul_f32")) {
+    const DType mdt = std::string(pw) == "matmul_f32" ? DType::F32 : DType::BF16;
     const int64_t M = 128, K = 64, N = 128;
     const int nb = 256;  // distinct operand sets, reused round robin
-    TensorView QA = rt.alloc_tensor(DType::BF16, {int64_t{nb} * M * K});
-    TensorView KB = rt.alloc_tensor(DType::BF16, {int64_t{nb} * N * K});
-    TensorView OS = rt.alloc_tensor(DType::BF16, {int64_t{n} * M * N});
+    TensorView QA = rt.alloc_tensor(mdt, {int64_t{nb} * M * K});
+    TensorView KB = rt.alloc_tensor(mdt, {int64_t{nb} * N * K});
+    TensorView OS = rt.alloc_tensor(mdt, {int64_t{n} * M * N});
     for (int r = 0; r < reps; ++r) {
       for (int i = 0; i < n; ++i) {
         TensorView a2 = QA, b2 = KB, o2 = OS;
@@ -76,8 +77,8 @@ int main(int argc, char** argv) {
       float ms = 0;
       check_abi(gpuos_dev_run_finite(rt.device(), &ms), "run_finite");
       const double flops = 2.0 * M * N * K * n;
-      std::printf("{\"tasks\": %d, \"op\": \"matmul_bf16 128x64x128\", \"kernel_ms\": %.4f, \"tasks_per_s\": %.1f, "
-                  "\"TFLOPs\": %.3f}\n", n, ms, n / (ms / 1e3), flops / (ms / 1e3) / 1e12);
+      std::printf("{\"tasks\": %d, \"op\": \"%s 128x64x128\", \"kernel_ms\": %.4f, \"tasks_per_s\": %.1f, "
+                  "\"TFLOPs\": %.3f}\n", n, pw, ms, n / (ms / 1e3), flops / (ms / 1e3) / 1e12);
     }
     return 0;
   }
