@@ -74,4 +74,9 @@ build/probe/pingpong: tools/probe/pingpong.cu
 build/probe/%: tools/probe/%.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	@mkdir -p build/probe
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
-.PHONY: probes
+# latency-bisection build of the runtime (clock64 stamps between pipeline
+# points, printed by the completer): build/dbg/libgpuos_cuda.so, used by
+# tools/lat_stamps.sh in place of the product library on the GPU box
+lat-debug:
+	$(MAKE) lib NVEXTRA=-DGPUOS_LAT_STAMPS OBJ=build/dbg LIBDIR=build/dbg
+.PHONY: probes lat-debug
