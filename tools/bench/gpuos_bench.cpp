@@ -143,7 +143,8 @@ int gb_step(void* h, int mode, double* out) {
       // (copy stream) overlaps the tasks of chunk k, and the D2H of every
       // finished chunk (second copy stream) overlaps both, so the step is
       // bounded by the H2D volume over PCIe rather than H2D + D2H in series.
-      const int chunks = 16;
+      const char* ce = std::getenv("GB_E2E_CHUNKS");
+      const int chunks = ce ? std::max(1, std::atoi(ce)) : 16;
       const int per = (b->n + chunks - 1) / chunks;
       const BufferPool::Buffer& ba = rt.pool().lookup(b->A.buffer);
       const BufferPool::Buffer& bb = rt.pool().lookup(b->B.buffer);
