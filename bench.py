@@ -100,6 +100,26 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
+def launch_replicas(n_gpus: int) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks of this script
+    (one process per GPU, torchrun's env contract, rendezvous on 127.0.0.1)
+    and relay rank 0's line.  Under torchrun RANK is already set."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n_gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n_gpus), LOCAL_WORLD_SIZE=str(n_gpus),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=subprocess.PIPE if r == 0 else subprocess.DEVNULL))
+    out = procs[0].communicate()[0].decode()
+    rc = max(p.wait() for p in procs)
+    sys.stdout.write(out)
+    return rc
+
+
 def dist_setup(n_gpus: int):
     if n_gpus <= 1 or "RANK" not in os.environ:
         return None, 0, 1, 0
@@ -123,6 +143,31 @@ def dist_max(dist, x: float) -> float:
 def dist_barrier(dist):
     if dist is not None:
         dist.barrier()
+
+
+def dist_gather(dist, x: float) -> list:
+    """Every rank's value of x (rank order)."""
+    if dist is None:
+        return [x]
+    import torch
+    out = [torch.zeros(1, dtype=torch.float64) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, torch.tensor([x], dtype=torch.float64))
+    return [float(t.item()) for t in out]
+
+
+def dist_sum(dist, x: float) -> float:
+    return sum(dist_gather(dist, x))
+
+
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+
+
+def load_checker(lib) -> bool:
+    """Parity leg: hand the oracle (test-only CPU restatement, pinned to the
+    reference by tests/) to the bench library as the checker.  It runs only
+    after timed regions, on outputs poisoned before the verified step."""
+    lib.gb_set_oracle.argtypes = [C.c_char_p]
+    return os.path.exists(ORACLE_SO) and lib.gb_set_oracle(ORACLE_SO.encode()) == 0
 
 
 def ref_cpu_baseline(seconds: float, steps: int = 0) -> dict | None:
@@ -166,28 +211,111 @@ def run_reference(args) -> None:
     print(json.dumps(line))
 
 
-def run_configs(lib, local: int) -> dict:
-    """BASELINE.json configs 2-4 on this GPU (tools/bench/gpuos_bench_configs.cpp)."""
+def parity_dict(vals, checked_what: str) -> dict:
+    """[mismatched tasks, checked tasks, checked elements, float-sum bit-exact
+    share, mismatched elements] from the bench library (put_tally)."""
+    if vals[0] < 0:
+        return {"checked": 0, "note": "no checker (oracle/liboracle.so missing)"}
+    return {"mismatches": int(vals[0]), "checked": int(vals[1]), "checked_elements": int(vals[2]),
+            "float_sum_bitexact_frac": vals[3], "mismatched_elements": int(vals[4]), "what": checked_what}
+
+
+def run_config5(lib, dist, rank: int, world: int, local: int, tasks_per_stream: int, streams: int = 8) -> dict:
+    """Config 5: `streams` independent config-2 streams, stream s on GPU s mod G
+    (G = world); every rank builds its streams, a barrier, then all ranks run
+    their streams concurrently; device time = max over ranks of each rank's
+    union of worker-kernel lifetimes.  At G > 1 the same streams also run at
+    G = 1 (all on rank 0's GPU) for rate(G) / (G * rate(1))."""
+    peaks = load_peaks()
+    lib.gb_c5_open.restype = C.c_void_p
+    lib.gb_c5_open.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_longlong]
+    lib.gb_c5_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_c5_survivors.argtypes = [C.c_void_p]
+    lib.gb_c5_survivors.restype = C.c_double
+    lib.gb_c5_close.argtypes = [C.c_void_p]
+    out_cap = 1 << 27  # output-ring elements per dtype per stream
+
+    def run(g: int, active: bool, verify: int):
+        mine = [s for s in range(streams) if s % g == rank] if active else []
+        n = len(mine)
+        res = (C.c_double * 16)()
+        h = None
+        if n:
+            workers = max(1, 148 // n)
+            ids = (C.c_int * n)(*mine)
+            h = lib.gb_c5_open(local, ids, n, tasks_per_stream, workers, out_cap)
+        dist_barrier(dist)
+        if h:
+            lib.gb_c5_run(h, 1, verify, res)
+        ms = res[1] if n else 0.0
+        surv = lib.gb_c5_survivors(h) if h else 0.0
+        if h:
+            lib.gb_c5_close(h)
+        tot_ms = dist_max(dist, ms)
+        tasks = dist_sum(dist, res[0] if n else 0.0)
+        byts = dist_sum(dist, res[2] if n else 0.0)
+        failed = dist_sum(dist, res[3] if n else 0.0)
+        par = [dist_sum(dist, res[4 + i] if n else 0.0) for i in (0, 1, 2)] + [0.0]
+        par.append(dist_sum(dist, res[8] if n else 0.0))
+        se = dist_sum(dist, res[2 + 4] * res[3 + 4] if n else 0.0)  # bit-exact share, element-weighted
+        par[3] = se / par[2] if par[2] else 1.0
+        if not verify:
+            par = [-1.0] * 5
+        per_rank_ms = dist_gather(dist, ms)
+        surv_all = dist_sum(dist, surv)
+        return {"tasks": tasks, "ms": tot_ms, "bytes": byts, "failed": failed, "parity": par,
+                "per_rank_ms": per_rank_ms, "survivors": surv_all, "submit_ns": res[9] if n else 0.0}
+
+    r = run(world, True, 1)
+    g = world
+    rate = r["tasks"] / (r["ms"] / 1e3)
+    gbps = r["bytes"] / (r["ms"] / 1e3) / 1e9
+    res = {
+        "workload": f"{streams} independent config-2 streams (seeds 42..{41 + streams}) x {tasks_per_stream:,} mixed "
+                    f"micro-ops, stream s on GPU s mod G (G={g}), one host producer thread and one runtime (ring + "
+                    f"persistent generation of {148 // max(1, -(-streams // g))} CTAs) per stream; device time = union "
+                    "of the streams' worker-kernel lifetimes, max over GPUs",
+        "G": g, "tasks_per_s": rate, "alg_GBps": gbps,
+        "roofline_frac_per_gpu": gbps / (g * peaks["hbm_gbs"]), "failed_tasks": int(r["failed"]),
+        "union_ms": r["ms"], "per_gpu_ms": r["per_rank_ms"], "host_submit_ns_per_task": r["submit_ns"],
+        "parity": parity_dict(r["parity"], f"surviving outputs of the output rings ({int(r['survivors']):,} of "
+                                           f"{int(r['tasks']):,} tasks; each output region is reused every "
+                                           f"{out_cap:,} elements of its dtype)"),
+    }
+    if g > 1:
+        r1 = run(1, rank == 0, 0)
+        rate1 = r1["tasks"] / (r1["ms"] / 1e3)
+        res["rate_G1_tasks_per_s"] = rate1
+        res["scaling_efficiency"] = rate / (g * rate1)
+    return res
+
+
+def run_configs(lib, local: int, tasks2: int, tasks5: int) -> dict:
+    """BASELINE.json configs 2-4 on this GPU (tools/bench/gpuos_bench_configs.cpp),
+    each verified against the oracle after its timed steps."""
     peaks = load_peaks()
     lib.gb_config2.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_config3.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_config4.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
-    out = (C.c_double * 16)()
+    out = (C.c_double * 32)()
     res = {}
-    lib.gb_config2(local, 20_000, 3, out)
+    lib.gb_config2(local, tasks2, 3, out)
     res["config2_mixed"] = {
         "workload": "mixed {add,mul,relu,reduce_sum} x {f32,f16,bf16,i32}, numel log-uniform 64..65536, "
-                    "contiguous/strided/broadcast layouts, seed 42; 20,000 tasks per step, distinct outputs",
+                    f"contiguous/strided/broadcast layouts, seed 42; {tasks2:,} tasks per step, distinct outputs",
         "tasks_per_s": out[0], "alg_GBps": out[1], "roofline_frac": out[1] / peaks["hbm_gbs"],
-        "mean_bytes_per_task": out[3], "failed_tasks": int(out[4]), "host_submit_ns_per_task": out[5]}
+        "mean_bytes_per_task": out[3], "failed_tasks": int(out[4]), "host_submit_ns_per_task": out[5],
+        "parity": parity_dict(list(out[6:11]), "every task of the last timed step (outputs poisoned before it)")}
     for name, dt in (("config3_attention_f32", 0), ("config3_attention_bf16", 4)):
         lib.gb_config3(local, dt, 20, out)
         res[name] = {
             "workload": "32 heads x seq 128 x head_dim 64: Q*scale, Q.K^T (transposed view), softmax, P.V as "
                         "128 individual tasks per step, host waits between the 4 phases",
             "step_us": out[0], "tasks_per_s": out[1], "gflops": out[2], "failed_tasks": int(out[3]),
-            "max_rel_err_head0": out[4],
-            "phase_us": {"scale": out[5], "qk_t": out[6], "softmax": out[7], "pv": out[8]}}
+            "max_rel_err": out[4],
+            "phase_us": {"scale": out[5], "qk_t": out[6], "softmax": out[7], "pv": out[8]},
+            "parity": parity_dict(list(out[9:14]), "all 32 heads x 4 phases of the last step vs the oracle on "
+                                                   "that phase's GPU inputs")}
     lib.gb_config4(local, 1_000_000, out)
     res["config4_hot_swap"] = {
         "workload": "1,000,000 fp32 4096-element tasks alternating builtin add and injected scale_add(1.5,-0.25); "
@@ -198,14 +326,6 @@ def run_configs(lib, local: int) -> dict:
         "window_rows_checked": int(out[6]), "rows_not_one_variant": int(out[7]),
         "old_rows_past_window": int(out[8]), "failed_tasks": int(out[9]), "canary_hits": int(out[10]),
         "old_rows": int(out[11]), "new_rows": int(out[12])}
-    lib.gb_config5.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
-    lib.gb_config5(local, 8, 50_000, 18, out)
-    res["config5_streams_1gpu"] = {
-        "workload": "8 independent config-2 streams (seeds 42..49) x 50,000 mixed micro-ops, one host producer "
-                    "thread and one runtime (ring + persistent generation of 18 CTAs) per stream, all on this GPU "
-                    "(G=1 of the 1/2/4/8 sharding; bench.py --gpus G runs one replica per GPU)",
-        "tasks_per_s": out[0], "alg_GBps": out[1], "roofline_frac": out[1] / peaks["hbm_gbs"],
-        "failed_tasks": int(out[2]), "slowest_stream_ms": out[3]}
     lib.gb_native.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_native(local, 200_000, out)
     res["config4_native_promotion"] = {
@@ -229,8 +349,12 @@ def main() -> None:
     ap.add_argument("--capacity", type=int, default=4096)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2-4 lines")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs 2-5 lines")
+    ap.add_argument("--config2-tasks", type=int, default=1_000_000)
+    ap.add_argument("--config5-tasks", type=int, default=1_000_000, help="tasks per stream")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        sys.exit(launch_replicas(args.gpus))
     if args.impl == "reference":
         run_reference(args)
         return
@@ -241,11 +365,14 @@ def main() -> None:
     if not os.path.exists(lib_path):
         raise SystemExit("libgpuos_bench.so not built: run __graft_entry__.build()")
     lib = C.CDLL(lib_path)
+    checker = load_checker(lib)
     lib.gb_open.restype = C.c_void_p
     lib.gb_open.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
     lib.gb_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double)]
     lib.gb_latency.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_verify.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_int]
+    lib.gb_poison.argtypes = [C.c_void_p]
+    lib.gb_checker.argtypes = [C.c_void_p]
     lib.gb_info.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
     lib.gb_close.argtypes = [C.c_void_p]
 
@@ -259,22 +386,31 @@ def main() -> None:
 
     for _ in range(args.warmup):
         step(0)
-    dist_barrier(dist)
+    dev_ms, host_ms, sub_ms, fallbacks = [], [], [], 0
+    bad_total, checked_total = 0, 0
+    bad, checked = C.c_uint64(), C.c_uint64()
     clocks = ClockSampler(local)
     clocks.start()
-    dev_ms, host_ms, sub_ms, fallbacks = [], [], [], 0
     for _ in range(args.steps):
+        # outputs poisoned (NaN) before every timed step and checked after it,
+        # both outside the CUDA-event-timed worker-kernel lifetime
+        lib.gb_poison(h)
+        dist_barrier(dist)
         d, hm, fb, sm = step(0)
         dev_ms.append(d)
         host_ms.append(hm)
         sub_ms.append(sm)
         fallbacks += int(fb)
+        lib.gb_verify(h, C.byref(bad), C.byref(checked), 0)
+        bad_total += bad.value
+        checked_total += checked.value
     clk = clocks.stop()
     dist_barrier(dist)
     total_dev_s = dist_max(dist, sum(dev_ms) / 1e3)
     total_host_s = dist_max(dist, sum(host_ms) / 1e3)
-    bad, checked = C.c_uint64(), C.c_uint64()
-    lib.gb_verify(h, C.byref(bad), C.byref(checked), 0)
+    per_rank_ms = dist_gather(dist, 1e3 * sum(dev_ms) / 1e3 / args.steps)
+    bad_all = dist_sum(dist, float(bad_total))
+    checked_all = dist_sum(dist, float(checked_total))
 
     # baseline (a): one cudaLaunchKernel per task, same bodies
     base_steps = max(1, min(args.steps, 3))
@@ -286,15 +422,30 @@ def main() -> None:
     p50, p99 = lat[0], lat[1]
     lib.gb_latency(h, 1, 2_000, 200, lat)
     lp50, lp99 = lat[0], lat[1]
-    # e2e arm: host buffers, copies inside the timed region
+    # e2e arm: host buffers, copies inside the timed region (host outputs
+    # poisoned before every step, checked after the last)
     step(2)
-    e2e_ms = [step(2)[1] for _ in range(max(1, min(args.steps, 5)))]
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        lib.gb_poison(h)
+        e2e_ms.append(step(2)[1])
     e_bad, e_checked = C.c_uint64(), C.c_uint64()
     lib.gb_verify(h, C.byref(e_bad), C.byref(e_checked), 1)
+    e2e_rate = N_TASKS / (statistics.median(e2e_ms) / 1e3)
+    e2e_total = dist_sum(dist, e2e_rate)  # independent replicas: rates add
     info = C.create_string_buffer(512)
     lib.gb_info(h, info, 512)
+    oracle_checked = bool(lib.gb_checker(h))
     lib.gb_close(h)
-    configs = None if (args.no_configs or world > 1) else run_configs(lib, local)
+    configs = None
+    if not args.no_configs:
+        if world == 1:
+            configs = run_configs(lib, local, args.config2_tasks, args.config5_tasks)
+        else:
+            configs = {"note": "configs 2-4 are single-GPU workloads, measured at --gpus 1"}
+        c5 = run_config5(lib, dist, rank, world, local, args.config5_tasks)
+        if rank == 0:
+            configs["config5_streams"] = c5
 
     if rank != 0:
         dist_barrier(dist)
@@ -310,7 +461,6 @@ def main() -> None:
         with open(tp) as f:
             traffic = json.load(f).get("bytes_per_step")
     base_value = N_TASKS / (statistics.median(b_dev) / 1e3)
-    e2e_value = N_TASKS / (statistics.median(e2e_ms) / 1e3)
     cpu = None
     if not args.no_cpu_baseline:
         r = ref_cpu_baseline(seconds=args.cpu_seconds)
@@ -322,23 +472,29 @@ def main() -> None:
         "warmup": args.warmup, "ms_per_step": per_step_dev_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "tasks_per_step": N_TASKS, "elems": N_ELEMS, "global_batch": N_TASKS * world,
-                   "l2": "inputs larger than L2 (491.5 MB distinct buffers per step)",
+                   "l2": "inputs larger than L2 (491.5 MB distinct buffers per step; outputs poisoned between steps)",
                    "buffers": "device memory (RuntimeConfig::device_buffers); e2e copies pinned host <-> device",
                    "parallelism": f"independent ring + persistent kernel per GPU x{world}",
                    "runtime": json.loads(info.value.decode())},
+        "per_gpu_ms_per_step": per_rank_ms,
         "p50_submit_to_complete_us": p50, "p99_submit_to_complete_us": p99,
         "host_clock_tasks_per_s": tasks_total / total_host_s,
         "host_submit_ns_per_task": 1e6 * statistics.median(sub_ms) / N_TASKS,
         "baseline_per_op_launch": {"value": base_value, "unit": "tasks/s", "p50_launch_sync_us": lp50,
-                                   "p99_launch_sync_us": lp99, "speedup": value / base_value},
+                                   "p99_launch_sync_us": lp99, "speedup": value / (base_value * world)},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
-                     "kernel": "gpuos_worker_kernel (per step: 10,000 x 49,152 algorithmic bytes)"},
+                     "kernel": "gpuos_worker_kernel (per step: 10,000 x 49,152 algorithmic bytes, slowest GPU)"},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "tasks/s", "h2d_bytes_per_step": 2 * N_TASKS * N_ELEMS * 4,
-                "d2h_bytes_per_step": N_TASKS * N_ELEMS * 4},
-        "gpu_launches": args.steps,
-        "parity": {"mismatches": bad.value, "checked": checked.value, "e2e_mismatches": e_bad.value},
+        "e2e": {"value": e2e_total, "unit": "tasks/s", "h2d_bytes_per_step": 2 * N_TASKS * N_ELEMS * 4 * world,
+                "d2h_bytes_per_step": N_TASKS * N_ELEMS * 4 * world},
+        "gpu_launches": args.steps * world,
+        "parity": {"mismatches": int(bad_all), "checked": int(checked_all), "e2e_mismatches": e_bad.value,
+                   "e2e_checked": e_checked.value,
+                   "what": "every output element of every timed step (poisoned before the step) vs the "
+                           + ("oracle's add" if oracle_checked else "host f32(a + b) (oracle not loaded: "
+                                                                   "oracle/liboracle.so missing)")},
+        "checker": "oracle/liboracle.so" if checker else None,
         "queue_full_fallbacks": fallbacks,
         "configs": configs,
         "clocks": clk,

@@ -188,6 +188,11 @@ typedef struct gpuos_cfg {
  * config-1 e2e tasks/s); BufferPool::data<T>() pointers are then device
  * pointers, so host access goes through upload/download. */
 #define GPUOS_CFG_DEVICE_BUFFERS 0x1ull
+/* gpuos_cfg.flags: open without a resident generation (as env
+ * GPUOS_DEFER_START=1): work published before gpuos_dev_run_finite is drained
+ * by one finite generation, which profilers that serialise kernel launches
+ * (ncu) can capture; gpuos_dev_start makes it persistent. */
+#define GPUOS_CFG_DEFER_START 0x2ull
 
 typedef struct gpuos_dev gpuos_dev; /* opaque per-GPU runtime */
 
@@ -279,6 +284,10 @@ int gpuos_buf_free(gpuos_dev* dev, uint64_t id);
 int gpuos_buf_lookup(gpuos_dev* dev, uint64_t id, int* dtype, uint64_t* n, void** ptr);
 /* dir: 0 = host->device, 1 = device->host, 2 = device->device; synchronous on a side stream. */
 int gpuos_buf_copy(gpuos_dev* dev, void* dst, const void* src, uint64_t bytes, int dir);
+/* Fill `bytes` bytes at `dst` (buffer memory) with `byte` on the side stream,
+ * synchronously.  Benchmarks poison outputs (0xff: NaN) before a verified
+ * step so stale results cannot pass the check (BufferPool::fill). */
+int gpuos_buf_fill(gpuos_dev* dev, void* dst, int byte, uint64_t bytes);
 /* Migrate a buffer's pages to HBM ahead of a timed run. */
 int gpuos_buf_prefetch(gpuos_dev* dev, uint64_t id);
 /* Fill a view descriptor for buffer `id` (resolves addr, status, bounds). */

@@ -24,6 +24,7 @@ DTYPE_NAMES = {F32: "f32", F64: "f64", I32: "i32", F16: "f16", BF16: "bf16"}
 MAX_INPUTS, MAX_SCALARS, MAX_RANK = 4, 8, 4
 SLOT_BYTES = 384
 FLAG_FUSED, FLAG_SHUTDOWN, FLAG_UNCAPPED = 0x1, 0x2, 0x4
+CFG_DEVICE_BUFFERS, CFG_DEFER_START = 0x1, 0x2
 KIND_PROGRAM, KIND_KILLED = 64, 65
 FIRST_INJECTED_ID = 32
 
@@ -100,7 +101,7 @@ EXPORTS = [
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
     "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_ring_submit_dense", "gpuos_event_done", "gpuos_jit_compile_object", "gpuos_jit_link_worker",
     "gpuos_dev_load_native", "gpuos_table_install_native", "gpuos_program_upload", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
-    "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
+    "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_fill", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
     "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
     "gpuos_table_install_builtin", "gpuos_table_install_program", "gpuos_table_kill",
@@ -150,6 +151,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_buf_free": ([P, U64], I),
         "gpuos_buf_lookup": ([P, U64, C.POINTER(I), C.POINTER(U64), C.POINTER(P)], I),
         "gpuos_buf_copy": ([P, P, P, U64, I], I),
+        "gpuos_buf_fill": ([P, P, I, U64], I),
         "gpuos_buf_prefetch": ([P, U64], I),
         "gpuos_view_bind": ([P, U64, I, C.c_int64, I, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                              C.POINTER(View)], I),
@@ -229,12 +231,14 @@ class Device:
 
     def __init__(self, device: int = 0, capacity: int = 4096, num_workers: int = 0, telemetry: bool = True,
                  table_slots: int = 1024, trace_capacity: int = 65536, install_builtins: bool = True,
-                 cells: int = 1 << 16):
+                 cells: int = 1 << 16, defer_start: bool = False):
         self.lib = load_library()
         cfg = Cfg()
         self.lib.gpuos_default_cfg(C.byref(cfg))
         cfg.capacity, cfg.num_workers, cfg.telemetry = capacity, num_workers, int(telemetry)
         cfg.table_slots, cfg.trace_capacity = table_slots, trace_capacity
+        if defer_start:
+            cfg.flags |= CFG_DEFER_START
         h = C.c_void_p()
         _ck(self.lib.gpuos_dev_open(device, C.byref(cfg), C.byref(h)), "dev_open")
         self.h = h
@@ -270,6 +274,13 @@ class Device:
 
     def start(self) -> int:
         return self.lib.gpuos_dev_start(self.h)
+
+    def run_finite(self) -> float:
+        """With no resident generation: drain everything published so far with
+        one finite worker generation (sentinel behind it); returns its kernel ms."""
+        ms = C.c_float()
+        _ck(self.lib.gpuos_dev_run_finite(self.h, C.byref(ms)), "run_finite")
+        return ms.value
 
     def hold(self, on: bool) -> None:
         _ck(self.lib.gpuos_dev_hold(self.h, int(on)), "hold")

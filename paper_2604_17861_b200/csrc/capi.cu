@@ -503,7 +503,7 @@ int gpuos_dev_open(int device, const gpuos_cfg* cfg_in, gpuos_dev** out) {
   // gpuos_dev_run_finite (profilers serialise launches, so a persistent
   // generation launched here would never return under ncu).
   const char* defer = std::getenv("GPUOS_DEFER_START");
-  if (!(defer && defer[0] == '1')) {
+  if (!(defer && defer[0] == '1') && !(cfg.flags & GPUOS_CFG_DEFER_START)) {
     rc = launch_workers(d.get());
     if (rc) return rc;
   }
@@ -733,6 +733,14 @@ int gpuos_buf_copy(gpuos_dev* d, void* dst, const void* src, uint64_t bytes, int
   cudaSetDevice(d->device);
   const cudaMemcpyKind k = dir == 0 ? cudaMemcpyHostToDevice : dir == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   GPUOS_CK(cudaMemcpyAsync(dst, src, bytes, k, d->side));
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  return GPUOS_OK;
+}
+
+int gpuos_buf_fill(gpuos_dev* d, void* dst, int byte, uint64_t bytes) {
+  if (!d || (!dst && bytes)) return GPUOS_INTERNAL;
+  cudaSetDevice(d->device);
+  GPUOS_CK(cudaMemsetAsync(dst, byte & 0xff, bytes, d->side));
   GPUOS_CK(cudaStreamSynchronize(d->side));
   return GPUOS_OK;
 }
@@ -1664,13 +1672,17 @@ int gpuos_dev_load_native(gpuos_dev* d, const void* cubin, size_t size, const ui
     if (rc) return rc;
   }
   const uint64_t t1 = steady_ns();
+  // Every failure after the drain relaunches the previous generation (its
+  // module and jit table are untouched), so the ring keeps a consumer.
+  auto fail = [&](CUmodule m, int code) {
+    if (m) D.unload(m);
+    if (was_running) gpuos_dev_start(d);
+    return code;
+  };
   CUmodule mod = nullptr;
-  if (D.load(&mod, cubin) != CUDA_SUCCESS) return GPUOS_VERIFY_ERROR;
+  if (D.load(&mod, cubin) != CUDA_SUCCESS) return fail(nullptr, GPUOS_VERIFY_ERROR);
   CUfunction fn = nullptr;
-  if (D.get_fn(&fn, mod, "gpuos_worker_kernel") != CUDA_SUCCESS) {
-    D.unload(mod);
-    return GPUOS_VERIFY_ERROR;
-  }
+  if (D.get_fn(&fn, mod, "gpuos_worker_kernel") != CUDA_SUCCESS) return fail(mod, GPUOS_VERIFY_ERROR);
   D.fn_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)d->smem);
   D.fn_attr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, gdev::smem_carveout());
   std::vector<void*> table(gdev::kJitSlots, nullptr);
@@ -1678,13 +1690,13 @@ int gpuos_dev_load_native(gpuos_dev* d, const void* cubin, size_t size, const ui
     CUdeviceptr gp = 0;
     size_t gs = 0;
     if (slots[i] >= gdev::kJitSlots || D.get_global(&gp, &gs, mod, ptr_syms[i]) != CUDA_SUCCESS || gs != 8 ||
-        D.dtoh(&table[slots[i]], gp, 8) != CUDA_SUCCESS) {
-      D.unload(mod);
-      return GPUOS_VERIFY_ERROR;
-    }
+        D.dtoh(&table[slots[i]], gp, 8) != CUDA_SUCCESS)
+      return fail(mod, GPUOS_VERIFY_ERROR);
   }
-  GPUOS_CK(cudaMemcpyAsync(d->jit_dev, table.data(), table.size() * sizeof(void*), cudaMemcpyHostToDevice, d->side));
-  GPUOS_CK(cudaStreamSynchronize(d->side));
+  if (cudaMemcpyAsync(d->jit_dev, table.data(), table.size() * sizeof(void*), cudaMemcpyHostToDevice, d->side) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(d->side) != cudaSuccess)
+    return fail(mod, GPUOS_INTERNAL);
   if (d->native_mod) D.unload((CUmodule)d->native_mod);
   d->native_mod = mod;
   d->native_fn = fn;

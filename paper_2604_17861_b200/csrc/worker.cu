@@ -624,23 +624,26 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
 __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHeader* H, const gpuos_task* task,
                                               const SharedCtl* ctl, int code, uint64_t t_end, uint64_t& executed) {
   asm volatile("fence.release.gpu;" ::: "memory");
-  if (task->done_cell) {
-    const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (task->seq << 16);
-    st_relaxed_sys((uint64_t*)task->done_cell, word);
-  }
+  const uint64_t state = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8);
   if ((task->flags & GPUOS_FLAG_FUSED_COMPOSITE) && task->n_scalars > 1) {
-    // the chain's earlier steps complete with the composite: their (cell,
-    // seq) pairs sit in a host-written record (scalars[1])
+    // the chain's earlier steps complete with the composite, in chain order
+    // and before the composite's own cell (runtime.hpp:904-908): their (cell,
+    // seq) pairs sit in a host-written record (scalars[1]) that the host may
+    // reuse once the final cell is posted, so it is read first
     const uint64_t* rec = (const uint64_t*)__double_as_longlong(task->scalars[1]);
     if (rec) {
       const uint64_t nsteps = ld_relaxed_sys(rec);
       for (uint64_t k = 0; k < nsteps && k < GPUOS_MAX_FUSED; ++k) {
         const uint64_t cell = ld_relaxed_sys(rec + 1 + 2 * k), seq = ld_relaxed_sys(rec + 2 + 2 * k);
-        const uint64_t word = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8) | (seq << 16);
-        st_relaxed_sys((uint64_t*)cell, word);
+        st_relaxed_sys((uint64_t*)cell, state | (seq << 16));
       }
+      // the composite's own cell is released after the earlier ones
+      if (task->done_cell) st_release_sys((uint64_t*)task->done_cell, state | (task->seq << 16));
+      goto counted;
     }
   }
+  if (task->done_cell) st_relaxed_sys((uint64_t*)task->done_cell, state | (task->seq << 16));
+counted:
   *(volatile uint64_t*)&H->done = H->done + 1;
   atomicAdd((unsigned long long*)&S->processed, 1ull);
   if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);

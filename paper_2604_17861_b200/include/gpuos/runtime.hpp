@@ -14,6 +14,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -104,30 +105,38 @@ class CellPool {
  public:
   static constexpr uint32_t kBlockBits = 16;
   static constexpr uint32_t kBlock = 1u << kBlockBits;
+  /// Blocks live at fixed addresses for the pool's lifetime: the producer
+  /// appends (grow) while any thread may wait on a handle, so readers index a
+  /// fixed array of atomically published Block pointers, never a container
+  /// that could reallocate under them.  256 blocks = 16M live cells.
+  static constexpr uint32_t kMaxBlocks = 256;
 
   explicit CellPool(gpuos_dev* dev) : dev_(dev) { grow(); }
 
-  uint64_t* word(uint32_t g) const { return blocks_[g >> kBlockBits].host + (g & (kBlock - 1)); }
+  uint64_t* word(uint32_t g) const {
+    return blk(g)->host.load(std::memory_order_acquire) + (g & (kBlock - 1));
+  }
 
   /// Completion record of cell g for fused composites (mapped pinned, 32
   /// words: n, then (cell device address, seq) pairs); allocated per block
-  /// on first use.  Only the composite's final cell owns one, and a cell is
-  /// not reused before its task completes, so records never race.
+  /// on first use.  Only the composite's final cell owns one; the device reads
+  /// the record before it posts that final cell, and a cell (with its record)
+  /// is not reused before its task completes, so records never race.
   static constexpr uint32_t kRecordWords = 32;
   uint64_t* record(uint32_t g, uint64_t* device_addr) {
-    Block& b = blocks_[g >> kBlockBits];
+    Block& b = *blk(g);
     if (!b.rec_host) check_abi(gpuos_cells_alloc(dev_, kBlock * kRecordWords, &b.rec_host, &b.rec_dev), "records");
     const uint64_t i = g & (kBlock - 1);
     *device_addr = b.rec_dev + 8ull * kRecordWords * i;
     return b.rec_host + kRecordWords * i;
   }
-  uint64_t device_addr(uint32_t g) const { return blocks_[g >> kBlockBits].dev + 8ull * (g & (kBlock - 1)); }
+  uint64_t device_addr(uint32_t g) const { return blk(g)->dev + 8ull * (g & (kBlock - 1)); }
 
   /// Producer thread only.  A cell is reusable when no handle references it
   /// and its previous task's completion (tagged with that task's seq) has
   /// landed; words are seq-tagged, so a reused cell needs no clearing store.
   uint32_t acquire(uint64_t seq) {
-    const uint32_t total = static_cast<uint32_t>(blocks_.size()) * kBlock;
+    const uint32_t total = nblocks_.load(std::memory_order_relaxed) * kBlock;
     for (int probe = 0; probe < 64; ++probe) {
       const uint32_t g = cursor_;
       cursor_ = (cursor_ + 1) % total;
@@ -135,12 +144,12 @@ class CellPool {
         const uint32_t ahead = (g + 32) % total;
         _mm_prefetch(reinterpret_cast<const char*>(word(ahead)), _MM_HINT_T0);
       }
-      Block& b = blocks_[g >> kBlockBits];
+      Block& b = *blk(g);
       const uint32_t i = g & (kBlock - 1);
       if (b.refs[i].load(std::memory_order_acquire) != 0) continue;
       const uint64_t prev = b.last_seq[i];
       if (prev != 0) {
-        const uint64_t w = __atomic_load_n(&b.host[i], __ATOMIC_ACQUIRE);
+        const uint64_t w = __atomic_load_n(&b.host.load(std::memory_order_relaxed)[i], __ATOMIC_ACQUIRE);
         if ((w & 0xffu) == 0 || (w >> 16) != (prev & kSeqMask)) continue;  // previous task in flight
       }
       b.last_seq[i] = seq;
@@ -149,27 +158,27 @@ class CellPool {
       b.refs[i].store(1, std::memory_order_relaxed);
       return g;
     }
-    cursor_ = static_cast<uint32_t>(blocks_.size()) * kBlock;
+    cursor_ = nblocks_.load(std::memory_order_relaxed) * kBlock;
     grow();
     const uint32_t g = cursor_;
-    cursor_ = (cursor_ + 1) % (static_cast<uint32_t>(blocks_.size()) * kBlock);
-    blocks_[g >> kBlockBits].last_seq[g & (kBlock - 1)] = seq;
-    blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].store(1, std::memory_order_relaxed);
+    cursor_ = (cursor_ + 1) % (nblocks_.load(std::memory_order_relaxed) * kBlock);
+    blk(g)->last_seq[g & (kBlock - 1)] = seq;
+    blk(g)->refs[g & (kBlock - 1)].store(1, std::memory_order_relaxed);
     return g;
   }
   static constexpr uint64_t kSeqMask = (uint64_t{1} << 48) - 1;
   // One atomic per handle copy/destroy: the pool's own lifetime after the
   // runtime is gone is derived from the per-cell counts (try_delete), not
   // from a second shared counter.
-  void addref(uint32_t g) { blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_add(1, std::memory_order_relaxed); }
+  void addref(uint32_t g) { blk(g)->refs[g & (kBlock - 1)].fetch_add(1, std::memory_order_relaxed); }
   void release(uint32_t g) {
     // seq_cst pairs with orphan(): the last releaser or orphan() sees the other
-    if (blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].fetch_sub(1, std::memory_order_seq_cst) == 1 &&
+    if (blk(g)->refs[g & (kBlock - 1)].fetch_sub(1, std::memory_order_seq_cst) == 1 &&
         orphaned_.load(std::memory_order_seq_cst))
       try_delete();
   }
   long use_count(uint32_t g) const {
-    return static_cast<long>(blocks_[g >> kBlockBits].refs[g & (kBlock - 1)].load(std::memory_order_relaxed));
+    return static_cast<long>(blk(g)->refs[g & (kBlock - 1)].load(std::memory_order_relaxed));
   }
   /// Host-side completion (inline / validation / shutdown paths).
   void complete(uint32_t g, uint64_t seq, ErrorCode c) {
@@ -177,56 +186,82 @@ class CellPool {
     __atomic_store_n(word(g), w, __ATOMIC_RELEASE);
   }
   /// Before the device memory goes away: copy words to the heap, then free
-  /// ourselves when the last handle drops.
+  /// ourselves when the last handle drops.  Readers switch to the heap copy
+  /// through the atomic host pointer.
   void orphan() {
-    for (Block& b : blocks_) {
+    const uint32_t n = nblocks_.load(std::memory_order_acquire);
+    for (uint32_t k = 0; k < n; ++k) {
+      Block& b = *blocks_[k].load(std::memory_order_acquire);
       uint64_t* h = new uint64_t[kBlock];
-      std::memcpy(h, b.host, kBlock * 8);
-      b.host = h;
-      b.heap = true;
+      std::memcpy(h, b.host.load(std::memory_order_relaxed), kBlock * 8);
+      b.heap = h;
+      b.host.store(h, std::memory_order_release);
     }
     orphaned_.store(true, std::memory_order_seq_cst);
     try_delete();
   }
   ~CellPool() {
-    for (Block& b : blocks_) {
-      if (b.heap) delete[] b.host;
-      delete[] b.refs;
-      delete[] b.last_seq;
+    const uint32_t n = nblocks_.load(std::memory_order_acquire);
+    for (uint32_t k = 0; k < n; ++k) {
+      Block* b = blocks_[k].load(std::memory_order_acquire);
+      delete[] b->heap;
+      delete[] b->refs;
+      delete[] b->last_seq;
+      delete b;
     }
+  }
+  uint32_t blocks() const { return nblocks_.load(std::memory_order_acquire); }
+  /// Intentional no-consumer windows (generation handovers, shutdown) nest.
+  void pause(int delta) { paused_.fetch_add(delta, std::memory_order_acq_rel); }
+  /// True when no worker generation is resident outside an intentional
+  /// window: a waiter on a pending cell would otherwise spin forever.
+  bool consumer_lost() const {
+    if (orphaned_.load(std::memory_order_acquire) || paused_.load(std::memory_order_acquire) > 0) return false;
+    return gpuos_dev_alive(dev_) == 0 && paused_.load(std::memory_order_acquire) == 0;
   }
 
  private:
   struct Block {
-    uint64_t* host = nullptr;
+    std::atomic<uint64_t*> host{nullptr};
     uint64_t dev = 0;
     std::atomic<uint32_t>* refs = nullptr;
     uint64_t* last_seq = nullptr;  // seq of the cell's latest task, 0 = never used
     uint64_t* rec_host = nullptr;  // fused-composite completion records (lazily)
     uint64_t rec_dev = 0;
-    bool heap = false;
+    uint64_t* heap = nullptr;      // orphaned copy of the words
   };
+  Block* blk(uint32_t g) const { return blocks_[g >> kBlockBits].load(std::memory_order_acquire); }
   void grow() {
-    Block b;
-    check_abi(gpuos_cells_alloc(dev_, kBlock, &b.host, &b.dev), "cells");
-    b.refs = new std::atomic<uint32_t>[kBlock]();
-    b.last_seq = new uint64_t[kBlock]();
-    blocks_.push_back(b);
+    const uint32_t n = nblocks_.load(std::memory_order_relaxed);
+    if (n >= kMaxBlocks) throw Error(ErrorCode::Internal, "completion cells exhausted (16M live handles)");
+    Block* b = new Block;
+    uint64_t* host = nullptr;
+    check_abi(gpuos_cells_alloc(dev_, kBlock, &host, &b->dev), "cells");
+    b->host.store(host, std::memory_order_relaxed);
+    b->refs = new std::atomic<uint32_t>[kBlock]();
+    b->last_seq = new uint64_t[kBlock]();
+    blocks_[n].store(b, std::memory_order_release);  // published before any cell of it is handed out
+    nblocks_.store(n + 1, std::memory_order_release);
   }
 
   // After orphan(): delete once no handle references any cell.
   void try_delete() {
-    for (const Block& b : blocks_)
+    const uint32_t n = nblocks_.load(std::memory_order_acquire);
+    for (uint32_t k = 0; k < n; ++k) {
+      const Block& b = *blocks_[k].load(std::memory_order_acquire);
       for (uint32_t i = 0; i < kBlock; ++i)
         if (b.refs[i].load(std::memory_order_seq_cst) != 0) return;
+    }
     if (!deleting_.exchange(true, std::memory_order_acq_rel)) delete this;
   }
 
   gpuos_dev* dev_;
-  std::vector<Block> blocks_;
+  std::array<std::atomic<Block*>, kMaxBlocks> blocks_{};
+  std::atomic<uint32_t> nblocks_{0};
   uint32_t cursor_ = 0;
   std::atomic<bool> orphaned_{false};
   std::atomic<bool> deleting_{false};
+  std::atomic<int> paused_{0};
 };
 
 }  // namespace detail
@@ -271,9 +306,12 @@ class TaskHandle {
     if ((w & 0xffu) != static_cast<uint64_t>(TaskState::Failed)) return ErrorCode::Ok;
     return static_cast<ErrorCode>((w >> 8) & 0xffu);
   }
-  /// Block until terminal: spin, then yield, then sleep.
+  /// Block until terminal: spin, then yield, then sleep.  Throws
+  /// RuntimeStopped when the worker generation is gone (twice, ~10 ms apart)
+  /// while the task is still pending, instead of spinning forever.
   TaskState wait() const {
     uint64_t w = raw();
+    int lost = 0;
     for (uint32_t spin = 0; (w & 0xffu) == 0; ++spin) {
       if (spin < 2048) {
         __builtin_ia32_pause();
@@ -281,6 +319,11 @@ class TaskHandle {
         std::this_thread::yield();
       } else {
         std::this_thread::sleep_for(std::chrono::microseconds(10));
+        if ((spin & 1023) == 0) {
+          lost = pool_->consumer_lost() ? lost + 1 : 0;
+          if (lost >= 2 && (raw() & 0xffu) == 0)
+            throw Error(ErrorCode::RuntimeStopped, "worker generation stopped with the task pending");
+        }
       }
       w = raw();
     }
@@ -627,8 +670,10 @@ class Runtime {
     if (rc != 0) throw Error(static_cast<ErrorCode>(rc), "native link failed: " + std::string(log.c_str()));
     std::vector<const char*> sym_ptrs;
     for (const std::string& x : syms) sym_ptrs.push_back(x.c_str());
+    cells_->pause(1);  // the handover's drain/relaunch window
     rc = gpuos_dev_load_native(dev_, cubin, csize, slots.data(), sym_ptrs.data(), static_cast<int>(slots.size()),
                                &st.handover);
+    cells_->pause(-1);
     gpuos_free(cubin);
     if (rc != 0) throw Error(static_cast<ErrorCode>(rc), "native module load failed");
     InjectionRecord meta;
@@ -653,6 +698,8 @@ class Runtime {
   void wait_all() {
     if (!chain_.empty()) flush_chain();
     const int rc = gpuos_ring_wait_processed(dev_, committed_tasks_);
+    if (rc == static_cast<int>(ErrorCode::RuntimeStopped) && !stopped_)
+      throw Error(ErrorCode::RuntimeStopped, "worker generation stopped with tasks pending");
     if (rc != 0 && rc != static_cast<int>(ErrorCode::RuntimeStopped)) check_abi(rc, "wait_all");
   }
   TaskQueue::Snapshot peek_queue() const {
@@ -724,6 +771,7 @@ class Runtime {
     flush_chain();
     wait_all();
     stopped_ = true;
+    cells_->pause(1);  // stays paused: every committed task completed above
     gpuos_dev_stop(dev_);
     pool_->clear();
   }
@@ -733,8 +781,12 @@ class Runtime {
   /// kernel lifetime with CUDA events.
   void restart_workers() {
     wait_all();
-    check_abi(gpuos_dev_stop(dev_), "stop");
-    check_abi(gpuos_dev_start(dev_), "start");
+    cells_->pause(1);
+    const int rc = gpuos_dev_stop(dev_);
+    const int rc2 = rc ? rc : gpuos_dev_start(dev_);
+    cells_->pause(-1);
+    check_abi(rc, "stop");
+    check_abi(rc2, "start");
   }
 
  private:

@@ -459,6 +459,19 @@ class BufferPool {
     if (dev_) check_abi(gpuos_buf_copy(dev_, dst, b.data, bytes, 1), "download");
     else std::memcpy(dst, b.data, bytes);
   }
+  /// Bytes [byte_off, byte_off + bytes) of a buffer to the host.
+  void download_range(BufferId id, size_t byte_off, void* dst, size_t bytes) const {
+    const Buffer& b = lookup(id);
+    if (dev_) check_abi(gpuos_buf_copy(dev_, dst, static_cast<const char*>(b.data) + byte_off, bytes, 1), "download");
+    else std::memcpy(dst, static_cast<const char*>(b.data) + byte_off, bytes);
+  }
+  /// Byte fill of the whole buffer (benchmarks poison outputs with 0xff = NaN).
+  void fill(BufferId id, int byte) {
+    Buffer& b = const_cast<Buffer&>(lookup(id));
+    const size_t bytes = b.length * dtype_width(b.dtype);
+    if (dev_) check_abi(gpuos_buf_fill(dev_, b.data, byte, bytes), "fill");
+    else std::memset(b.data, byte, bytes);
+  }
   void prefetch(BufferId id) {
     if (dev_) check_abi(gpuos_buf_prefetch(dev_, dev_ids_[id]), "prefetch");
   }

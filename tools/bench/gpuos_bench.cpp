@@ -18,6 +18,8 @@
 #include <gpuos/runtime.hpp>
 #include <immintrin.h>
 
+#include "oracle_check.hpp"
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -49,7 +51,8 @@ struct Bench {
   void* cstream = nullptr;   // copy stream (H2D)
   void* dstream = nullptr;   // copy stream (D2H)
   void* ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  std::vector<float> expect;  // host reference of c = a + b (f32 add), for the self-check
+  std::vector<float> expect;  // expected c = a + b: the oracle's add once loaded (f32(a + b) before)
+  bool expect_from_oracle = false;
   uint64_t last_fallbacks = 0;
 };
 
@@ -330,10 +333,26 @@ int gb_latency(void* h, int mode, int samples, int warmup, double* out) {
   return 0;
 }
 
+// Poison the outputs before a verified step (0xff bytes = NaN): the device
+// copy, and for the e2e arm also the pinned host copy the D2H lands in.
+int gb_poison(void* h) {
+  auto* b = static_cast<Bench*>(h);
+  b->rt->pool().fill(b->Cv.buffer, 0xff);
+  std::memset(b->hC, 0xff, static_cast<size_t>(b->n) * b->e * 4);
+  return 0;
+}
+
 // Bit-exact self-check of every output element against f32(a + b).
 int gb_verify(void* h, uint64_t* mismatches, uint64_t* checked, int from_host_copy) {
   auto* b = static_cast<Bench*>(h);
   const uint64_t total = static_cast<uint64_t>(b->n) * b->e;
+  if (gbcheck::oracle().ok && !b->expect_from_oracle) {  // the checker's add over the same inputs
+    const int64_t t = static_cast<int64_t>(total);
+    orc_view o = gbcheck::view(b->expect.data(), ORC_F32, 0, {t}, {1});
+    orc_view in[2] = {gbcheck::view(b->hA, ORC_F32, 0, {t}, {1}), gbcheck::view(b->hB, ORC_F32, 0, {t}, {1})};
+    if (gbcheck::oracle().elementwise(0, &o, in, 2) != 0) return 1;
+    b->expect_from_oracle = true;
+  }
   std::vector<float> got(total);
   if (from_host_copy) std::memcpy(got.data(), b->hC, total * 4);
   else b->rt->pool().download(b->Cv.buffer, got.data(), total * 4);
@@ -342,10 +361,10 @@ int gb_verify(void* h, uint64_t* mismatches, uint64_t* checked, int from_host_co
     if (std::memcmp(&got[i], &b->expect[i], 4) != 0) ++bad;
   *mismatches = bad;
   *checked = total;
-  // reset outputs so the next check sees fresh writes
-  std::memset(b->hC, 0, total * 4);
   return 0;
 }
+
+int gb_checker(void* h) { return static_cast<Bench*>(h)->expect_from_oracle ? 1 : 0; }
 
 int gb_info(void* h, char* buf, size_t cap) {
   auto* b = static_cast<Bench*>(h);
