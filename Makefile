@@ -28,7 +28,7 @@ $(LIBDIR)/gpuos_worker_rdc.cubin: $(CSRC)/worker.cu $(DEV_HDRS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -rdc=true -maxrregcount=80 -DGPUOS_WORKER_IMAGE -cubin $< -o $@
 bench: $(LIBDIR)/libgpuos_bench.so
-cpp-tests: build/cpp/test_runtime build/cpp/test_host
+cpp-tests: build/cpp/test_runtime build/cpp/test_host build/cpp/gates
 
 $(OBJ)/worker.o: $(CSRC)/worker.cu $(DEV_HDRS)
 	@mkdir -p $(OBJ)
@@ -57,6 +57,11 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib bench cpp-tests oracle clean
+
+# acceptance gates C6/C8/C9/C10 + the reference bench workloads on the GPU runtime
+build/cpp/gates: tools/bench/gpuos_gates.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
+	@mkdir -p build/cpp
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -lgpuos_cuda -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -lpthread
 
 build/cpp/test_host: tests/cpp/test_host.cpp tests/cpp/check.hpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 	@mkdir -p build/cpp

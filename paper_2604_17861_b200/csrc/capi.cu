@@ -545,11 +545,8 @@ int gpuos_dev_start(gpuos_dev* d) {
   s.hint = next;
   s.stop_pos = gdev::kRunning;
   // stream-ordered on the kernel stream, ahead of the launch: no host round
-  // trips between the caller's start and the generation (the source is the
-  // persistent shadow, so the async copies may still be in flight here)
-  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, claim), &s.claim, 8, cudaMemcpyHostToDevice, d->ks));
-  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, hint), &s.hint, 8, cudaMemcpyHostToDevice, d->ks));
-  GPUOS_CK(cudaMemcpyAsync((char*)d->S + offsetof(DevState, stop_pos), &s.stop_pos, 8, cudaMemcpyHostToDevice, d->ks));
+  // trips between the caller's start and the generation
+  GPUOS_CK(gdev::launch_gen_init(d->S, s.claim, s.hint, s.stop_pos, d->ks));
   return launch_workers(d);
 }
 

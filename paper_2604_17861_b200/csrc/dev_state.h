@@ -115,6 +115,9 @@ cudaError_t launch_worker(DevState* s, uint32_t workers, uint32_t threads, uint3
 cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32_t nparts,
                         uint32_t* counter, cudaStream_t st);
 cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st);
+// Stream-ordered generation start: claim/hint/stop_pos in one tiny launch
+// (three pageable 8-byte copies cost more stream time than the launch).
+cudaError_t launch_gen_init(DevState* s, uint64_t claim, uint64_t hint, uint64_t stop_pos, cudaStream_t st);
 uint32_t worker_smem_bytes();
 uint32_t worker_threads();
 int smem_carveout();  // preferred shared carveout (percent) for every kernel, GPUOS_CARVEOUT overrides

@@ -939,6 +939,12 @@ __global__ void __launch_bounds__(256, 3) gpuos_task_kernel(const gpuos_task tas
 
 __global__ void gpuos_clock_probe(uint64_t* out) { out[0] = globaltimer(); }
 
+__global__ void gpuos_gen_init(DevState* S, uint64_t claim, uint64_t hint, uint64_t stop_pos) {
+  S->claim = claim;
+  S->hint = hint;
+  S->stop_pos = stop_pos;
+}
+
 typedef void (*TaskKernel)(const gpuos_task, uint64_t, uint32_t*);
 
 static TaskKernel task_kernel_for(uint32_t kind) {
@@ -993,6 +999,7 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
     cudaFuncGetAttributes(&fa, f);
   }
   cudaFuncGetAttributes(&fa, gpuos_clock_probe);
+  cudaFuncGetAttributes(&fa, gpuos_gen_init);
 }
 
 cudaError_t worker_occupancy(int* per_sm) {
@@ -1013,6 +1020,11 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
 
 cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st) {
   gpuos_clock_probe<<<1, 1, 0, st>>>(out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_init(DevState* s, uint64_t claim, uint64_t hint, uint64_t stop_pos, cudaStream_t st) {
+  gpuos_gen_init<<<1, 1, 0, st>>>(s, claim, hint, stop_pos);
   return cudaGetLastError();
 }
 

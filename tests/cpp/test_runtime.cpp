@@ -5,6 +5,7 @@
 // drain-on-shutdown.  Built by `make cpp-tests`, run by tests/test_cpp_gpu.py.
 #include <gpuos/runtime.hpp>
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <random>
@@ -462,6 +463,104 @@ TEST_CASE("accounting identity holds at quiescence") {
   CHECK(c.submitted == c.inline_executions + c.committed + rt.fusion_absorbed());
   CHECK(c.processed == c.committed);
   CHECK(c.failed == 1);
+  const auto s = rt.peek_queue();
+  CHECK(s.processed == s.head);
+  CHECK(s.head == s.tail);
+}
+
+// Reference C1 (acceptance_main.cpp:80-212) and test_queue.cpp:292-361 on the
+// device ring: a monitor thread samples peek_queue() continuously while one
+// producer streams 10^5 tasks through compact (dense) and extended
+// (broadcast scalar) slots; the cursor invariant processed <= head <= tail
+// must hold in every sample and every cursor must be monotone.  Exactly-once:
+// each task's output region is a function of its sequence number, every
+// handle completes Done, and the device trace holds every sequence number
+// exactly once (xor and count, as the reference checks).
+TEST_CASE("live ring invariants: processed <= head <= tail under load, every task exactly once") {
+  RuntimeConfig cfg = small_config(1024, 0);
+  cfg.telemetry_enabled = true;
+  const int n = 100000, len = 64;
+  cfg.trace_capacity = n + 1024;
+  Runtime rt(cfg);
+  auto x = rt.alloc_tensor(DType::F32, {len});
+  auto consts = rt.alloc_tensor(DType::F32, {n});
+  auto out = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  std::vector<double> xv(len), cv(n);
+  for (int i = 0; i < len; ++i) xv[i] = i * 0.5;
+  for (int i = 0; i < n; ++i) cv[i] = static_cast<double>(i % 4096);
+  fill(rt, x, xv);
+  fill(rt, consts, cv);
+  std::atomic<bool> stop{false};
+  std::atomic<uint64_t> samples{0}, violations{0}, regressions{0};
+  std::thread monitor([&] {
+    TaskQueue::Snapshot last{};
+    while (!stop.load(std::memory_order_acquire)) {
+      const TaskQueue::Snapshot s = rt.peek_queue();
+      if (!(s.processed <= s.head && s.head <= s.tail)) violations.fetch_add(1);
+      if (s.processed < last.processed || s.head < last.head || s.tail < last.tail) regressions.fetch_add(1);
+      last = s;
+      samples.fetch_add(1);
+    }
+  });
+  std::vector<TaskHandle> hs;
+  hs.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    TensorView o = out;
+    o.shape = {len};
+    o.strides = {1};
+    o.offset = int64_t{i} * len;
+    if (i % 2 == 0) {
+      // compact slot: o = x * x (dense, same shape)
+      hs.push_back(rt.submit(OpKind::Mul, {x, x}, o));
+    } else {
+      // extended slot: o = x + consts[i] (rank-0 broadcast view)
+      TensorView c = consts;
+      c.shape = {};
+      c.strides = {};
+      c.offset = i;
+      hs.push_back(rt.submit(OpKind::Add, {x, c}, o));
+    }
+  }
+  rt.wait_all();
+  stop.store(true, std::memory_order_release);
+  monitor.join();
+  std::printf("  %llu peek samples during the run\n", (unsigned long long)samples.load());
+  CHECK(samples.load() > 100);
+  CHECK(violations.load() == 0);
+  CHECK(regressions.load() == 0);
+  uint64_t not_done = 0, xor_want = 0;
+  for (const TaskHandle& h : hs) {
+    not_done += h.state() == TaskState::Done ? 0 : 1;
+    xor_want ^= h.id();
+  }
+  CHECK(not_done == 0);
+  const std::vector<double> got = read_all(rt, out);
+  uint64_t bad = 0;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < len; ++k) {
+      const double want = i % 2 == 0 ? f32(xv[k] * xv[k]) : f32(xv[k] + cv[i]);
+      bad += got[static_cast<size_t>(i) * len + k] == want ? 0 : 1;
+    }
+  CHECK(bad == 0);
+  const auto tr = rt.trace();
+  REQUIRE(tr.size() == static_cast<size_t>(n));
+  std::vector<uint8_t> seen(static_cast<size_t>(n) + 2, 0);
+  uint64_t xor_seen = 0, dup = 0, foreign = 0;
+  const uint64_t base = hs.front().id();
+  for (const Tracepoint& t : tr) {
+    xor_seen ^= t.seq;
+    if (t.seq < base || t.seq - base >= static_cast<uint64_t>(n)) {
+      ++foreign;
+      continue;
+    }
+    dup += seen[t.seq - base]++ ? 1 : 0;
+  }
+  CHECK(dup == 0);
+  CHECK(foreign == 0);
+  CHECK(xor_seen == xor_want);
+  const CounterSnapshot c = rt.counters();
+  CHECK(c.processed == c.committed);
+  CHECK(c.committed == static_cast<uint64_t>(n));
   const auto s = rt.peek_queue();
   CHECK(s.processed == s.head);
   CHECK(s.head == s.tail);

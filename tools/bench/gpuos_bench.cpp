@@ -225,6 +225,21 @@ int gb_step(void* h, int mode, double* out) {
                    "%.2f p90 %.2f | done p50 %.2f | ticket->seen p50 %.2f us\n",
                    (unsigned long long)n, (last - first) / 1e6, pct(enq_seen, .5), pct(enq_seen, .9), pct(seen_deq, .5),
                    pct(seen_deq, .9), pct(exec, .5), pct(exec, .9), pct(done, .5), pct(tick, .5));
+      // step timeline: tasks enqueued / seen / done per 25 us bucket, from
+      // the first ticket (the generation's first claim)
+      uint64_t t_first = UINT64_MAX;
+      for (uint64_t i = 0; i < n; ++i) t_first = std::min({t_first, ph[i].ticket_ns, ph[i].enqueue_ns});
+      const int nb = 48;
+      std::vector<int> enq(nb), seen(nb), dn(nb);
+      auto bk = [&](uint64_t t) { return std::min<int>(nb - 1, (int)((t - t_first) / 25000)); };
+      for (uint64_t i = 0; i < n; ++i) {
+        ++enq[bk(ph[i].enqueue_ns)];
+        ++seen[bk(ph[i].seen_ns)];
+        ++dn[bk(ph[i].done_ns)];
+      }
+      std::fprintf(stderr, "timeline (25 us buckets from the first claim/enqueue): enq/seen/done\n");
+      for (int k = 0; k < nb; ++k)
+        if (enq[k] || seen[k] || dn[k]) std::fprintf(stderr, "  %4d us: %5d %5d %5d\n", 25 * k, enq[k], seen[k], dn[k]);
     }
     float ms = 0;
     check_abi(gpuos_event_sync(b->dev, b->ev[1]), "sync ev1");

