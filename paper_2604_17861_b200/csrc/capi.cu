@@ -215,6 +215,9 @@ struct gpuos_dev {
   gdev::TraceRec* dtrace = nullptr;
   uint64_t trace_cap = 0;
   int64_t gt_offset = 0;   // host_ns = globaltimer + gt_offset
+  int64_t clk_rtt_ns = 0;  // round trip of the winning calibration round
+  uint64_t clk_at_ns = 0;  // steady time of the last calibration
+  char* clk_host = nullptr;  // mapped page of the clock ping-pong
   double tsc_per_ns = 1.0; // rdtsc -> steady ns conversion
   uint64_t tsc0 = 0, ns0 = 0;
   uint32_t* launch_counters = nullptr;
@@ -317,30 +320,56 @@ int gpuos_default_cfg(gpuos_cfg* cfg) {
   return GPUOS_OK;
 }
 
+// Host steady clock <-> device %globaltimer, and rdtsc -> steady ns.
+// Offset: a ping-pong through mapped memory (gpuos_clock_probe); the round
+// with the shortest round trip wins, so the error is at most half of it
+// (~1 us over PCIe).  TSC rate: measured over the longest baseline available
+// (device open -> now), so enqueue stamps stay aligned over long runs.  Run at
+// open and again before every trace export (the two clocks drift by ppm).
 static int calibrate_clocks(gpuos_dev* d) {
-  uint64_t* dbuf = nullptr;
-  GPUOS_CK(cudaMalloc(&dbuf, 8));
-  int64_t best_rtt = INT64_MAX;
-  for (int i = 0; i < 8; ++i) {
+  constexpr int kRounds = 16;
+  if (!d->clk_host) {
+    GPUOS_CK(cudaHostAlloc(&d->clk_host, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+    d->pinned_blocks.push_back(d->clk_host);  // freed at close with the ring
+  }
+  uint32_t* flag = reinterpret_cast<uint32_t*>(d->clk_host);
+  uint64_t* out = reinterpret_cast<uint64_t*>(d->clk_host + 64);
+  std::memset(d->clk_host, 0, 4096);
+  GPUOS_CK(gdev::launch_clock_probe(flag, out, kRounds, d->side));
+  int64_t best_rtt = INT64_MAX, off = d->gt_offset;
+  bool ok = true;
+  for (int r = 0; r < kRounds && ok; ++r) {
     const uint64_t h0 = steady_ns();
-    GPUOS_CK(gdev::launch_clock_probe(dbuf, d->side));
-    GPUOS_CK(cudaStreamSynchronize(d->side));
-    const uint64_t h1 = steady_ns();
+    __atomic_store_n(flag, (uint32_t)(r + 1), __ATOMIC_RELEASE);
     uint64_t gt = 0;
-    GPUOS_CK(cudaMemcpyAsync(&gt, dbuf, 8, cudaMemcpyDeviceToHost, d->side));
-    GPUOS_CK(cudaStreamSynchronize(d->side));
-    if ((int64_t)(h1 - h0) < best_rtt) {
+    while ((gt = __atomic_load_n(&out[r], __ATOMIC_ACQUIRE)) == 0) {
+      if (steady_ns() - h0 > 2000000000ull) {  // probe never started: keep the previous offset
+        ok = false;
+        break;
+      }
+    }
+    const uint64_t h1 = steady_ns();
+    if (ok && (int64_t)(h1 - h0) < best_rtt) {
       best_rtt = (int64_t)(h1 - h0);
-      d->gt_offset = (int64_t)((h0 + h1) / 2) - (int64_t)gt;
+      off = (int64_t)((h0 + h1) / 2) - (int64_t)gt;
     }
   }
-  d->dev_blocks.push_back(dbuf);  // freed at close (cudaFree blocks behind resident kernels)
-  // TSC rate for cheap enqueue stamps
-  d->tsc0 = __rdtsc();
-  d->ns0 = steady_ns();
-  std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  __atomic_store_n(flag, (uint32_t)(kRounds + 1), __ATOMIC_RELEASE);  // release any waiting round
+  GPUOS_CK(cudaStreamSynchronize(d->side));
+  if (ok) {
+    d->gt_offset = off;
+    d->clk_rtt_ns = best_rtt;
+  }
   const uint64_t t1 = __rdtsc(), n1 = steady_ns();
-  d->tsc_per_ns = (double)(t1 - d->tsc0) / (double)(n1 - d->ns0);
+  if (d->tsc0 == 0) {
+    d->tsc0 = t1;
+    d->ns0 = n1;
+    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    d->tsc_per_ns = (double)(__rdtsc() - d->tsc0) / (double)(steady_ns() - d->ns0);
+  } else if (n1 - d->ns0 > 5000000ull) {
+    d->tsc_per_ns = (double)(t1 - d->tsc0) / (double)(n1 - d->ns0);
+  }
+  d->clk_at_ns = steady_ns();
   return GPUOS_OK;
 }
 
@@ -1268,6 +1297,7 @@ int gpuos_trace_enable(gpuos_dev* d, int on) {
 int gpuos_trace_snapshot(gpuos_dev* d, gpuos_tracepoint* out, uint64_t cap, uint64_t* n) {
   if (!d || !n) return GPUOS_INTERNAL;
   cudaSetDevice(d->device);
+  if (steady_ns() - d->clk_at_ns > 50000000ull) calibrate_clocks(d);  // fresh offset and TSC rate
   uint64_t head = 0;
   GPUOS_CK(cudaMemcpyAsync(&head, (char*)d->S + offsetof(DevState, trace_head), 8, cudaMemcpyDeviceToHost, d->side));
   std::vector<gdev::TraceRec> recs(d->trace_cap);
@@ -1297,6 +1327,7 @@ int gpuos_trace_snapshot(gpuos_dev* d, gpuos_tracepoint* out, uint64_t cap, uint
 int gpuos_trace_phases(gpuos_dev* d, gpuos_trace_phase* out, uint64_t cap, uint64_t* n) {
   if (!d || !n) return GPUOS_INTERNAL;
   cudaSetDevice(d->device);
+  if (steady_ns() - d->clk_at_ns > 50000000ull) calibrate_clocks(d);  // fresh offset and TSC rate
   uint64_t head = 0;
   GPUOS_CK(cudaMemcpyAsync(&head, (char*)d->S + offsetof(DevState, trace_head), 8, cudaMemcpyDeviceToHost, d->side));
   std::vector<gdev::TraceRec> recs(d->trace_cap);

@@ -24,7 +24,7 @@ constexpr uint32_t kJitKindBase = 96;
 constexpr uint32_t kJitSlots = 32;
 constexpr uint32_t kTaskBytes = 384;
 constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
-constexpr uint32_t kHeaderBytes = 5120;  // worker: task buffers, control blocks, counters, entry cache
+constexpr uint32_t kHeaderBytes = 7168;  // worker: task buffers, control blocks, counters, entry cache
 constexpr uint32_t kScratchBytes = 91 * 1024;
 constexpr uint32_t kLaunchCounters = 1u << 16;
 
@@ -114,7 +114,7 @@ void load_all_kernels(int* worker_regs, size_t* worker_local);
 cudaError_t launch_worker(DevState* s, uint32_t workers, uint32_t threads, uint32_t smem, cudaStream_t st);
 cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32_t nparts,
                         uint32_t* counter, cudaStream_t st);
-cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st);
+cudaError_t launch_clock_probe(const uint32_t* flag, uint64_t* out, int rounds, cudaStream_t st);
 // Stream-ordered generation start: claim/hint/stop_pos in one tiny launch
 // (three pageable 8-byte copies cost more stream time than the launch).
 cudaError_t launch_gen_init(DevState* s, uint64_t claim, uint64_t hint, uint64_t stop_pos, cudaStream_t st);

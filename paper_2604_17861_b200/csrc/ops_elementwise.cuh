@@ -249,14 +249,18 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
 }
 
 // Checks in the reference order (ops.hpp:133-153), then dispatch on dtype.
+template <int DT, class F>
+__device__ __forceinline__ void ew_dense_any(const gpuos_task* t, const Ctx* c, int64_t n, F f) {
+  ew_dense<DT>(t, c, n, f);
+}
 template <class F>
 __device__ __forceinline__ bool ew_dense_dispatch(const gpuos_task* t, const Ctx* c, int dt, int64_t n, F f) {
   switch (dt) {
-    case GPUOS_F32: ew_dense<GPUOS_F32>(t, c, n, f); return true;
-    case GPUOS_F64: ew_dense<GPUOS_F64>(t, c, n, f); return true;
-    case GPUOS_I32: ew_dense<GPUOS_I32>(t, c, n, f); return true;
-    case GPUOS_F16: ew_dense<GPUOS_F16>(t, c, n, f); return true;
-    case GPUOS_BF16: ew_dense<GPUOS_BF16>(t, c, n, f); return true;
+    case GPUOS_F32: ew_dense_any<GPUOS_F32>(t, c, n, f); return true;
+    case GPUOS_F64: ew_dense_any<GPUOS_F64>(t, c, n, f); return true;
+    case GPUOS_I32: ew_dense_any<GPUOS_I32>(t, c, n, f); return true;
+    case GPUOS_F16: ew_dense_any<GPUOS_F16>(t, c, n, f); return true;
+    case GPUOS_BF16: ew_dense_any<GPUOS_BF16>(t, c, n, f); return true;
     default: return false;
   }
 }
@@ -304,7 +308,7 @@ __device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
 #define GPUOS_EW_CASE(DT)                        \
   case DT:                                       \
     if (s.dense)                                 \
-      ew_dense<DT>(t, c, n, f);                  \
+      ew_dense_any<DT>(t, c, n, f);              \
     else                                         \
       ew_strided<DT>(t, c, s, n, f);             \
     break;
@@ -336,8 +340,10 @@ __device__ __forceinline__ int ew_entry(const gpuos_task* t, const Ctx* c, bool 
     const int64_t n = numel(t->views[0]);
     if (n > 0 && n < ((int64_t)1 << 31)) {
       F f;
-      // (a cp.async.bulk + mbarrier streaming variant measured slower than
-      // this register path at 4K, 16K and 64K elements: removed)
+      // (cp.async.bulk + mbarrier streaming variants were measured twice and
+      // dropped: slower at 4K-64K elements in round 1; a two-stage pipelined
+      // one hung on the box in round 2, while this register path already
+      // streams 64K-element tasks at 5.0 TB/s, profiles/r02_*)
       ew_dense<GPUOS_F32>(t, c, n, f);
       return GPUOS_OK;
     }

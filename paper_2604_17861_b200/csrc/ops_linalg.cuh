@@ -263,16 +263,121 @@ __device__ __noinline__ int op_sdpa(const gpuos_task* t, const Ctx* c) {
   if ((bc = bind_code(q)) || (bc = bind_code(kk)) || (bc = bind_code(vv)) || (bc = bind_code(out))) return bc;
   const int dt = out.dtype;
   const bool exact = exact_products(dt);
-  double* red = (double*)c->smem;           // 32 doubles
-  double* sc = red + 32;                    // score chunk
-  const int cap = (c->smem_bytes - 32 * 8) / 8;
-  const int chunk = cap < tl ? cap : tl;
-  const bool single = chunk >= tl;
   int64_t hlo, hhi;
   part_range(h, c->part, c->nparts, 1, &hlo, &hhi);
   const char* qp = (const char*)q.addr;
   const char* kp = (const char*)kk.addr;
   const char* vp = (const char*)vv.addr;
+  // Batched heads (decode attention: a few heads, d <= 256, contexts whose
+  // scores fit in scratch): the q rows and the scores of up to kHB heads sit in
+  // shared memory, each weight e_i / denom is formed once per key instead of
+  // once per (key, column), and the output columns of every head in the batch
+  // accumulate at once -- each thread carries up to four independent
+  // ascending-key chains.  Every value is computed in the reference's order
+  // (ascending j per score, ascending i per output column).
+  {
+    constexpr int kHB = 8;
+    const int nw = c->nthreads >> 5;
+    const int fixed = 8 * kHB + 2 * kHB + kHB * d;  // doubles: red, stats, q rows
+    const int avail = c->smem_bytes / 8 - fixed;
+    int hb = kHB;
+    if (avail / tl < hb) hb = avail / tl;
+    if ((4 * c->nthreads) / d < hb) hb = (4 * c->nthreads) / d;
+    if (d <= 256 && nw <= 8 && hb >= 1) {
+      double* red = (double*)c->smem;
+      double* stat = red + 8 * kHB;  // [0, kHB): max, [kHB, 2 kHB): denominator
+      double* qs = stat + 2 * kHB;
+      double* sc = qs + kHB * d;
+      for (int64_t h0 = hlo; h0 < hhi; h0 += hb) {
+        const int nb = (int)((hhi - h0) < hb ? (hhi - h0) : hb);
+        for (int e = c->tid; e < nb * d; e += c->nthreads) {
+          const int hh = e / d, j = e - hh * d;
+          qs[e] = load_any(dt, qp, (h0 + hh) * q.strides[0] + (int64_t)j * q.strides[1]);
+        }
+        group_sync(c);
+        // pass 1: scores and per-head max
+#pragma unroll 1
+        for (int hh = 0; hh < nb; ++hh) {
+          const int64_t kb = (h0 + hh) * kk.strides[0];
+          const double* qr = qs + hh * d;
+          double mx = -INFINITY;
+          for (int i = c->tid; i < tl; i += c->nthreads) {
+            const char* kr = kp;
+            const int64_t rb = kb + (int64_t)i * kk.strides[1];
+            double dot = 0.0;
+            for (int j = 0; j < d; ++j) dot = mac(dot, qr[j], load_any(dt, kr, rb + (int64_t)j * kk.strides[2]), exact);
+            const double sv = __dmul_rn(scale, dot);
+            sc[hh * tl + i] = sv;
+            mx = nan_skip_max(mx, sv);
+          }
+          for (int o = 16; o > 0; o >>= 1) mx = nan_skip_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          if ((c->tid & 31) == 0) red[(c->tid >> 5) * kHB + hh] = mx;
+        }
+        group_sync(c);
+        if (c->tid < nb) {
+          double mx = -INFINITY;
+          for (int w = 0; w < nw; ++w) mx = nan_skip_max(mx, red[w * kHB + c->tid]);
+          stat[c->tid] = mx;
+        }
+        group_sync(c);
+        // pass 2: e_i = exp(s_i - max) and the per-head denominators
+#pragma unroll 1
+        for (int hh = 0; hh < nb; ++hh) {
+          const double mx = stat[hh];
+          double sum = 0.0;
+          for (int i = c->tid; i < tl; i += c->nthreads) {
+            const double ev = exp(__dsub_rn(sc[hh * tl + i], mx));
+            sc[hh * tl + i] = ev;
+            sum += ev;
+          }
+          sum = warp_sum(sum);
+          if ((c->tid & 31) == 0) red[(c->tid >> 5) * kHB + hh] = sum;
+        }
+        group_sync(c);
+        if (c->tid < nb) {
+          double sum = 0.0;
+          for (int w = 0; w < nw; ++w) sum += red[w * kHB + c->tid];
+          stat[kHB + c->tid] = sum;
+        }
+        group_sync(c);
+        // weights w_i = e_i / denom, once per key
+        for (int e = c->tid; e < nb * tl; e += c->nthreads) {
+          const int hh = e / tl;
+          sc[e] = __ddiv_rn(sc[e], stat[kHB + hh]);
+        }
+        group_sync(c);
+        // pass 3: out[hh][j] = sum_i w_i * v[i][j], ascending i, four chains per thread
+        int ph[4], pj[4];
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const char* vb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int pidx = c->tid + r * c->nthreads;
+          ph[r] = pidx < nb * d ? pidx / d : -1;
+          pj[r] = pidx < nb * d ? pidx - ph[r] * d : 0;
+          vb[r] = vp + (ph[r] >= 0 ? ((h0 + ph[r]) * vv.strides[0] + (int64_t)pj[r] * vv.strides[2]) * dtype_width(dt) : 0);
+        }
+        const int64_t vstep = vv.strides[1];
+        for (int i = 0; i < tl; ++i) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (ph[r] >= 0)
+              acc[r] = __dadd_rn(acc[r], __dmul_rn(sc[ph[r] * tl + i], load_any(dt, vb[r], (int64_t)i * vstep)));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (ph[r] >= 0)
+            store_any(dt, (char*)out.addr, (h0 + ph[r]) * out.strides[0] + (int64_t)pj[r] * out.strides[1], acc[r]);
+        group_sync(c);
+      }
+      return GPUOS_OK;
+    }
+  }
+  double* red = (double*)c->smem;           // 32 doubles
+  double* sc = red + 32;                    // score chunk
+  const int cap = (c->smem_bytes - 32 * 8) / 8;
+  const int chunk = cap < tl ? cap : tl;
+  const bool single = chunk >= tl;
   for (int64_t head = hlo; head < hhi; ++head) {
     const int64_t qb = head * q.strides[0], kb = head * kk.strides[0], vb = head * vv.strides[0];
     auto score = [&](int i) {

@@ -98,13 +98,16 @@ constexpr int kWorkerRegs = 112;  // __maxnreg__ below; the inline dense path sp
 static_assert(((kWorkerThreads / 32 + 3) / 4) * kWorkerRegs * 32 + 2 * 80 * 32 <= 65536 / 4,
               "worker + task kernel exceed a sub-partition's register file");
 constexpr int kCompleterWarp = 1 + kGroups * kGroupThreads / 32;
-constexpr int kBufs = 4;
+constexpr int kBufs = 8;
 // Named barriers: 0 = whole CTA, 1+g = executor group g (task bodies),
-// FULL[b]  = 3+b  : fetcher arrives, group waits      (32 + 128)
-// DONE[b]  = 7+b  : group arrives, completer waits    (128 + 32)
-// EMPTY[b] = 11+b : completer arrives, fetcher waits  (32 + 32)
-constexpr int kBarFull = 3, kBarDone = 7, kBarEmpty = 11;
-constexpr int kFullCount = 32 + kGroupThreads, kDoneCount = kGroupThreads + 32, kEmptyCount = 64;
+// FULL[b] = 3+b (3..10): fetcher arrives, group waits (32 + 128).
+// DONE[b] and EMPTY[b] are shared-memory mbarriers (count 1): the group's
+// thread 0 arrives on DONE after its group barrier, the completer arrives on
+// EMPTY; phase parity = lap & 1.  mbarriers can be tested without blocking,
+// so the completer retires every consecutive finished buffer behind one
+// release fence.
+constexpr int kBarFull = 3;
+constexpr int kFullCount = 32 + kGroupThreads;
 constexpr int kMaxBatch = 4;  // tickets claimed per atomic / slots per warp-wide read
 constexpr uint64_t kSplitMin = 2048;  // output elements below which an idle split is not worth it
 constexpr uint32_t kTmemCols = 256;  // 128 per executor group; the rest stays free for standalone kernels
@@ -124,6 +127,22 @@ struct CachedEntry {
 };
 static_assert(sizeof(CachedEntry) == 32, "cache entry is 32 bytes");
 
+// Constant per generation: read once from DevState at kernel start into the
+// shared header (the fetcher reads it from there: in registers it pushed the
+// fetcher's loop past the register budget into local-memory spills)
+struct WConst {
+  const char* ring;
+  const char* ext;
+  uint64_t mask, cap;
+  const uint64_t* host_tail;
+  uint64_t* host_done;
+  uint64_t* host_claimed;
+  uint64_t* host_epoch;
+  uint64_t* dev_epoch;
+  TableEntry* bank[2];
+  uint32_t table_slots, spin_iterations, backoff_max_exp, num_workers;
+};
+
 // Shared header (kHeaderBytes): tasks | ctls | raw slot staging | counters | entry cache.
 struct WorkerHeader {
   gpuos_task task[kBufs];
@@ -132,10 +151,13 @@ struct WorkerHeader {
   uint64_t done;                        // tasks completed by this CTA (all generations)
   uint64_t claimed;                     // tickets claimed by this CTA (all generations)
   uint64_t mbar[kGroups];               // per-group tensor-core completion barriers
+  uint64_t done_bar[kBufs];             // DONE[b]: group -> completer
+  uint64_t empty_bar[kBufs];            // EMPTY[b]: completer -> fetcher
   uint32_t mma_phase[kGroups];
   uint32_t tmem_base;                   // kTmemCols columns, kTmemCols/kGroups per group
   uint32_t pad_;
   CachedEntry cache[kEntryCache];
+  WConst kc;
 #ifdef GPUOS_LAT_STAMPS
   long long dbg[16];  // latency bisection (debug builds only)
 #endif
@@ -164,7 +186,11 @@ __device__ __forceinline__ void buf_sync(int b) {
     case 0: bar_sync<BASE>(N); break;
     case 1: bar_sync<BASE + 1>(N); break;
     case 2: bar_sync<BASE + 2>(N); break;
-    default: bar_sync<BASE + 3>(N); break;
+    case 3: bar_sync<BASE + 3>(N); break;
+    case 4: bar_sync<BASE + 4>(N); break;
+    case 5: bar_sync<BASE + 5>(N); break;
+    case 6: bar_sync<BASE + 6>(N); break;
+    default: bar_sync<BASE + 7>(N); break;
   }
 }
 template <int BASE, int N>
@@ -173,28 +199,37 @@ __device__ __forceinline__ void buf_arrive(int b) {
     case 0: bar_arrive<BASE>(N); break;
     case 1: bar_arrive<BASE + 1>(N); break;
     case 2: bar_arrive<BASE + 2>(N); break;
-    default: bar_arrive<BASE + 3>(N); break;
+    case 3: bar_arrive<BASE + 3>(N); break;
+    case 4: bar_arrive<BASE + 4>(N); break;
+    case 5: bar_arrive<BASE + 5>(N); break;
+    case 6: bar_arrive<BASE + 6>(N); break;
+    default: bar_arrive<BASE + 7>(N); break;
   }
 }
-static_assert(kBufs == 4, "buf_sync/buf_arrive dispatch four buffers");
+static_assert(kBufs == 8 && kBarFull + kBufs <= 15, "buf_sync/buf_arrive dispatch eight buffers below barrier 15");
+
+// Shared-memory mbarrier arrive (release.cta) / non-blocking parity test.
+__device__ __forceinline__ void mbar_arrive1(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(mbar))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* mbar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"((uint32_t)__cvta_generic_to_shared(mbar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
-// Constant per generation: read once from DevState at kernel start.
-struct WConst {
-  const char* ring;
-  const char* ext;
-  uint64_t mask, cap;
-  const uint64_t* host_tail;
-  uint64_t* host_done;
-  uint64_t* host_claimed;
-  uint64_t* host_epoch;
-  uint64_t* dev_epoch;
-  TableEntry* bank[2];
-  uint32_t table_slots, spin_iterations, backoff_max_exp, num_workers;
-};
+
 
 // Publish-then-revalidate (executor.hpp:133-141): the epoch slot holds the
 // version dispatched under before any bank is read.
@@ -366,9 +401,9 @@ struct Fetcher {
 
 // Hand the next buffer to the executors: wait until the completer released
 // it (after its first lap), return its index.
-__device__ __forceinline__ int next_buffer(Fetcher& F) {
+__device__ __forceinline__ int next_buffer(WorkerHeader* H, Fetcher& F) {
   const int b = (int)(F.k % kBufs);
-  if (F.k >= (uint32_t)kBufs) buf_sync<kBarEmpty, kEmptyCount>(b);
+  if (F.k >= (uint32_t)kBufs) mbar_wait(&H->empty_bar[b], ((F.k / kBufs) - 1) & 1);
   return b;
 }
 
@@ -378,7 +413,7 @@ __device__ __forceinline__ int next_buffer(Fetcher& F) {
 __device__ __forceinline__ void fetcher_exit(const WConst& K, uint32_t w, WorkerHeader* H, Fetcher& F, int lane,
                                              bool first_marker_staged) {
   for (int g = first_marker_staged ? 1 : 0; g < kGroups; ++g) {
-    const int b = next_buffer(F);
+    const int b = next_buffer(H, F);
     if (lane == 0) {
       H->ctl[b].exit = 1;
       H->ctl[b].partial = 0;
@@ -388,7 +423,7 @@ __device__ __forceinline__ void fetcher_exit(const WConst& K, uint32_t w, Worker
     ++F.k;
   }
   const uint32_t inflight = F.k < (uint32_t)kBufs ? F.k : (uint32_t)kBufs;
-  for (uint32_t q = F.k - inflight; q < F.k; ++q) buf_sync<kBarEmpty, kEmptyCount>((int)(q % kBufs));
+  for (uint32_t q = F.k - inflight; q < F.k; ++q) mbar_wait(&H->empty_bar[q % kBufs], (q / kBufs) & 1);
   if (lane == 0) flush_mirror(K, w, F.mir, H->claimed, *(volatile uint64_t*)&H->done);
 }
 
@@ -404,37 +439,52 @@ __device__ __forceinline__ void fetcher_exit(const WConst& K, uint32_t w, Worker
 // near, and its poll carries the producer tail, so every publication
 // eventually advances the hint.
 __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint32_t w, int lane) {
-  WConst K;
-  K.ring = S->ring;
-  K.ext = S->ext;
-  K.mask = S->mask;
-  K.cap = S->cap;
-  K.host_tail = S->host_tail;
-  K.host_done = S->host_done;
-  K.host_claimed = S->host_claimed;
-  K.host_epoch = S->host_epoch;
-  K.dev_epoch = S->dev_epoch;
-  K.bank[0] = S->bank[0];
-  K.bank[1] = S->bank[1];
-  K.table_slots = S->table_slots;
-  K.spin_iterations = S->spin_iterations;
-  K.backoff_max_exp = S->backoff_max_exp;
-  K.num_workers = S->num_workers;
+  if (lane == 0) {
+    WConst& k = H->kc;
+    k.ring = S->ring;
+    k.ext = S->ext;
+    k.mask = S->mask;
+    k.cap = S->cap;
+    k.host_tail = S->host_tail;
+    k.host_done = S->host_done;
+    k.host_claimed = S->host_claimed;
+    k.host_epoch = S->host_epoch;
+    k.dev_epoch = S->dev_epoch;
+    k.bank[0] = S->bank[0];
+    k.bank[1] = S->bank[1];
+    k.table_slots = S->table_slots;
+    k.spin_iterations = S->spin_iterations;
+    k.backoff_max_exp = S->backoff_max_exp;
+    k.num_workers = S->num_workers;
+  }
+  __syncwarp();
+  const WConst& K = H->kc;
   Fetcher F;
   F.mir.flushed_claimed = H->claimed;
   F.mir.flushed_done = H->done;
   uint64_t last_pos = 0, hint_seen = ld_relaxed_gpu(&S->hint);
   const int seg = lane >> 3, sl = lane & 7;
+  // claim-ahead: the next batch's tickets are taken while the current batch is
+  // handed to the executors, so the HBM atomic's round trip overlaps staging
+  uint64_t pre_pos = 0;  // lane 0
+  uint32_t pre_nb = 0;   // lane 0
+  bool pre = false;      // warp-uniform
   for (;;) {
     // ---- claim a batch ----
     uint64_t pos = 0;
     uint32_t nb = 1;
     if (lane == 0) {
-      while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
-      nb = hint_seen > last_pos + 2ull * K.num_workers ? (uint32_t)kMaxBatch : 1u;
-      pos = atomicAdd((unsigned long long*)&S->claim, (unsigned long long)nb);
-      last_pos = pos + nb - 1;
+      if (pre) {
+        pos = pre_pos;
+        nb = pre_nb;
+      } else {
+        while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
+        nb = hint_seen > last_pos + 2ull * K.num_workers ? (uint32_t)kMaxBatch : 1u;
+        pos = atomicAdd((unsigned long long*)&S->claim, (unsigned long long)nb);
+        last_pos = pos + nb - 1;
+      }
     }
+    pre = false;
     pos = shfl64(pos, 0);
     nb = __shfl_sync(0xffffffffu, nb, 0);
     uint32_t j = 0;  // next slot of the batch to hand over
@@ -504,10 +554,21 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
           // stage the raw slots of the valid run
           if ((uint32_t)seg < ready) reinterpret_cast<uint4*>(H->raw[seg])[sl] = v;
           __syncwarp();
+          if (j + ready >= nb) {
+            // this round consumes the batch: take the next tickets now
+            uint32_t took = 0;
+            if (lane == 0 && !*(volatile uint32_t*)&S->hold && hint_seen > last_pos) {
+              pre_nb = hint_seen > last_pos + 2ull * K.num_workers ? (uint32_t)kMaxBatch : 1u;
+              pre_pos = atomicAdd((unsigned long long*)&S->claim, (unsigned long long)pre_nb);
+              last_pos = pre_pos + pre_nb - 1;
+              took = 1;
+            }
+            pre = __shfl_sync(0xffffffffu, took, 0) != 0;
+          }
           for (uint32_t i = 0; i < ready; ++i) {
             const uint64_t spos = pos + j;
             const uint64_t* raw = H->raw[i];
-            const int b = next_buffer(F);
+            const int b = next_buffer(H, F);
             gpuos_task* task = &H->task[b];
             SharedCtl* ctl = &H->ctl[b];
             const bool compact = (raw[6] & 0xff) == kFmtCompact;
@@ -576,7 +637,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             ++F.k;
             ++j;
             if (split) {
-              const int b2 = next_buffer(F);
+              const int b2 = next_buffer(H, F);
               if (lane < 24) reinterpret_cast<uint4*>(&H->task[b2])[lane] = reinterpret_cast<const uint4*>(task)[lane];
               if (lane < (int)(sizeof(SharedCtl) / 8))
                 reinterpret_cast<uint64_t*>(&H->ctl[b2])[lane] = reinterpret_cast<const uint64_t*>(ctl)[lane];
@@ -622,8 +683,8 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
 // release puts them in L2 (where the host's copy engine reads) before the
 // completion word is posted to host memory.
 __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHeader* H, const gpuos_task* task,
-                                              const SharedCtl* ctl, int code, uint64_t t_end, uint64_t& executed) {
-  asm volatile("fence.release.gpu;" ::: "memory");
+                                              const SharedCtl* ctl, int code, uint64_t t_end, uint64_t& executed,
+                                              uint32_t& n_done, uint32_t& n_failed) {
   const uint64_t state = ((uint64_t)(code == GPUOS_OK ? 1 : 2)) | ((uint64_t)(code & 0xff) << 8);
   if ((task->flags & GPUOS_FLAG_FUSED_COMPOSITE) && task->n_scalars > 1) {
     // the chain's earlier steps complete with the composite, in chain order
@@ -645,8 +706,8 @@ __device__ __forceinline__ void complete_task(DevState* S, uint32_t w, WorkerHea
   if (task->done_cell) st_relaxed_sys((uint64_t*)task->done_cell, state | (task->seq << 16));
 counted:
   *(volatile uint64_t*)&H->done = H->done + 1;
-  atomicAdd((unsigned long long*)&S->processed, 1ull);
-  if (code != GPUOS_OK) atomicAdd((unsigned long long*)&S->failed, 1ull);
+  ++n_done;
+  if (code != GPUOS_OK) ++n_failed;
   atomicAdd((unsigned long long*)&S->per_op[task->op_id < 256 ? task->op_id : 255], 1ull);
   if (ctl->trace_on) {
     const uint64_t ticket = atomicAdd((unsigned long long*)&S->trace_head, 1ull);
@@ -718,6 +779,10 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
       mbar_init(&H->mbar[g], 1);
       H->mma_phase[g] = 0;
     }
+    for (int b = 0; b < kBufs; ++b) {
+      mbar_init(&H->done_bar[b], 1);
+      mbar_init(&H->empty_bar[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc(&H->tmem_base, kTmemCols);  // owned (and released) by warp 1
@@ -730,34 +795,48 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
   }
   if (warp == kCompleterWarp) {
     // ---------------- completer: retires tasks in ticket order ----------------
+    // Lane 0 waits for the oldest buffer, then takes every consecutive buffer
+    // that is already done; one release fence orders all of their outputs
+    // before their completion words (the fence waits for the SM's
+    // outstanding writes, so one per run instead of one per task).
+    if (lane != 0) return;
     uint64_t executed = 0;
     int exits = 0;
-    for (uint32_t k = 0;; ++k) {
-      const int b = (int)(k % kBufs);
-      buf_sync<kBarDone, kDoneCount>(b);
-      const SharedCtl* ctl = &H->ctl[b];
-      if (ctl->exit) {
-        buf_arrive<kBarEmpty, kEmptyCount>(b);
-        if (++exits == kGroups) return;
-        continue;
-      }
-#ifdef GPUOS_LAT_STAMPS
-      if (lane == 0) LAT_STAMP(9);
-#endif
-      if (lane == 0 && !ctl->partial) complete_task(S, w, H, &H->task[b], ctl, ctl->code, ctl->t_end, executed);
-#ifdef GPUOS_LAT_STAMPS
-      if (lane == 0 && !ctl->partial) {
-        LAT_STAMP(10);
-        if (ctl->pos > 40 && ctl->pos % 37 == 0) {
-          const long long* d = H->dbg;
-          printf("LAT pos %llu size %lld part %d/%d: expand %lld plan+ctl %lld resolve %lld arrive %lld | wake %lld fnload %lld body %lld gsync %lld | done-wake %lld complete %lld\n",
-                 (unsigned long long)ctl->pos, (long long)H->task[b].size, ctl->part, ctl->nparts, d[1] - d[0], d[2] - d[1], d[3] - d[2],
-                 d[4] - d[3], d[5] - d[4], d[6] - d[5], d[7] - d[6], d[8] - d[7], d[9] - d[8], d[10] - d[9]);
+    for (uint32_t k = 0;;) {
+      mbar_wait(&H->done_bar[k % kBufs], (k / kBufs) & 1);
+      uint32_t n = 1;
+      while (n < (uint32_t)kBufs && mbar_test(&H->done_bar[(k + n) % kBufs], ((k + n) / kBufs) & 1)) ++n;
+      asm volatile("fence.release.gpu;" ::: "memory");
+      uint32_t n_done = 0, n_failed = 0;
+      for (uint32_t i = 0; i < n; ++i, ++k) {
+        const int b = (int)(k % kBufs);
+        const SharedCtl* ctl = &H->ctl[b];
+        if (ctl->exit) {
+          ++exits;
+          mbar_arrive1(&H->empty_bar[b]);
+          continue;
         }
-      }
+#ifdef GPUOS_LAT_STAMPS
+        LAT_STAMP(9);
 #endif
-      __syncwarp();
-      buf_arrive<kBarEmpty, kEmptyCount>(b);
+        if (!ctl->partial)
+          complete_task(S, w, H, &H->task[b], ctl, ctl->code, ctl->t_end, executed, n_done, n_failed);
+#ifdef GPUOS_LAT_STAMPS
+        if (!ctl->partial) {
+          LAT_STAMP(10);
+          if (ctl->pos > 40 && ctl->pos % 37 == 0) {
+            const long long* d = H->dbg;
+            printf("LAT pos %llu size %lld part %d/%d: expand %lld plan+ctl %lld resolve %lld arrive %lld | wake %lld fnload %lld body %lld gsync %lld | done-wake %lld complete %lld\n",
+                   (unsigned long long)ctl->pos, (long long)H->task[b].size, ctl->part, ctl->nparts, d[1] - d[0], d[2] - d[1], d[3] - d[2],
+                   d[4] - d[3], d[5] - d[4], d[6] - d[5], d[7] - d[6], d[8] - d[7], d[9] - d[8], d[10] - d[9]);
+          }
+        }
+#endif
+        mbar_arrive1(&H->empty_bar[b]);
+      }
+      if (n_done) atomicAdd((unsigned long long*)&S->processed, (unsigned long long)n_done);
+      if (n_failed) atomicAdd((unsigned long long*)&S->failed, (unsigned long long)n_failed);
+      if (exits == kGroups) return;
     }
   }
   // ---------------- executor group g: tasks g, g+2, g+4, ... ----------------
@@ -785,7 +864,7 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
     gpuos_task* task = &H->task[b];
     SharedCtl* ctl = &H->ctl[b];
     if (ctl->exit) {
-      buf_arrive<kBarDone, kDoneCount>(b);
+      if (ctx.tid == 0) mbar_arrive1(&H->done_bar[b]);
       // both groups are past their last tensor-core use: release TMEM
       tc_fence_before();
       bar_sync<kBarExecExit>(kGroups * kGroupThreads);
@@ -835,8 +914,8 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
       ctl->code = code;
       ctl->t_fenced = t_wake;
       ctl->t_end = globaltimer();
+      mbar_arrive1(&H->done_bar[b]);
     }
-    buf_arrive<kBarDone, kDoneCount>(b);
   }
 }
 
@@ -937,7 +1016,19 @@ __global__ void __launch_bounds__(256, 3) gpuos_task_kernel(const gpuos_task tas
   }
 }
 
-__global__ void gpuos_clock_probe(uint64_t* out) { out[0] = globaltimer(); }
+// Host <-> device clock ping-pong: round r waits for the host's flag to reach
+// r + 1 (mapped memory) and answers with %globaltimer; the host brackets each
+// round with its steady clock, so the offset error is half the round trip.
+__global__ void gpuos_clock_probe(const uint32_t* flag, uint64_t* out, int rounds) {
+  for (int r = 0; r < rounds; ++r) {
+    uint32_t f;
+    do {
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+    } while (f < (uint32_t)(r + 1));
+    const uint64_t t = globaltimer();
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(out + r), "l"(t) : "memory");
+  }
+}
 
 __global__ void gpuos_gen_init(DevState* S, uint64_t claim, uint64_t hint, uint64_t stop_pos) {
   S->claim = claim;
@@ -1018,8 +1109,8 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
   return cudaLaunchKernel((const void*)f, dim3(nparts), dim3(256), args, task_smem_bytes(), st);
 }
 
-cudaError_t launch_clock_probe(uint64_t* out, cudaStream_t st) {
-  gpuos_clock_probe<<<1, 1, 0, st>>>(out);
+cudaError_t launch_clock_probe(const uint32_t* flag, uint64_t* out, int rounds, cudaStream_t st) {
+  gpuos_clock_probe<<<1, 1, 0, st>>>(flag, out, rounds);
   return cudaGetLastError();
 }
 

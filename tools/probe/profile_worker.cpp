@@ -113,6 +113,29 @@ int main(int argc, char** argv) {
       std::sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.worker != b.worker ? a.worker < b.worker : a.ticket_ns < b.ticket_ns; });
       for (size_t i = 1; i < v.size(); ++i)
         if (v[i].worker == v[i - 1].worker) gaps.push_back((double)(int64_t)(v[i].ticket_ns - v[i - 1].ticket_ns) / 1e3);
+      // fetcher cadence inside a batch (same worker, same ticket stamp):
+      // seen -> first staged, and staged -> next staged (per-task handoff);
+      // and across batches: last staged -> next batch's ticket
+      std::vector<double> first_h, next_h, batch_gap, batch_n;
+      for (size_t i = 0; i < v.size();) {
+        size_t j = i;
+        std::vector<uint64_t> deq;
+        while (j < v.size() && v[j].worker == v[i].worker && v[j].ticket_ns == v[i].ticket_ns) deq.push_back(v[j++].dequeue_ns);
+        std::sort(deq.begin(), deq.end());
+        first_h.push_back((double)(int64_t)(deq[0] - v[i].seen_ns) / 1e3);
+        for (size_t k = 1; k < deq.size(); ++k) next_h.push_back((double)(int64_t)(deq[k] - deq[k - 1]) / 1e3);
+        batch_n.push_back((double)deq.size());
+        if (j < v.size() && v[j].worker == v[i].worker) batch_gap.push_back((double)(int64_t)(v[j].ticket_ns - deq.back()) / 1e3);
+        i = j;
+      }
+      auto med = [](std::vector<double> x, double q) {
+        std::sort(x.begin(), x.end());
+        return x.empty() ? 0.0 : x[static_cast<size_t>(q * (x.size() - 1))];
+      };
+      std::printf("  batch size mean %.2f | seen->first staged p50 %.2f p90 %.2f | staged->next staged p50 %.2f p90 %.2f"
+                  " | last staged->next ticket p50 %.2f p90 %.2f us\n",
+                  [&] { double t = 0; for (double x : batch_n) t += x; return batch_n.empty() ? 0.0 : t / batch_n.size(); }(),
+                  med(first_h, .5), med(first_h, .9), med(next_h, .5), med(next_h, .9), med(batch_gap, .5), med(batch_gap, .9));
       std::sort(gaps.begin(), gaps.end());
       if (!gaps.empty())
         std::printf("  ticket gap per worker p50 %.2f us p90 %.2f us\n", gaps[gaps.size() / 2], gaps[gaps.size() * 9 / 10]);
