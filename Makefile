@@ -84,4 +84,7 @@ build/probe/%: tools/probe/%.cpp $(HOST_HDRS) $(LIBDIR)/libgpuos_cuda.so
 # tools/lat_stamps.sh in place of the product library on the GPU box
 lat-debug:
 	$(MAKE) lib NVEXTRA=-DGPUOS_LAT_STAMPS OBJ=build/dbg LIBDIR=build/dbg
-.PHONY: probes lat-debug
+# fetcher hand-off cycle profile (build/fprof/libgpuos_cuda.so, swapped in by tools/fetch_prof.sh)
+fetch-prof:
+	$(MAKE) lib NVEXTRA=-DGPUOS_FETCH_PROF OBJ=build/fprof LIBDIR=build/fprof
+.PHONY: probes lat-debug fetch-prof

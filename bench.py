@@ -316,6 +316,17 @@ def run_configs(lib, local: int, tasks2: int, tasks5: int) -> dict:
             "phase_us": {"scale": out[5], "qk_t": out[6], "softmax": out[7], "pv": out[8]},
             "parity": parity_dict(list(out[9:14]), "all 32 heads x 4 phases of the last step vs the oracle on "
                                                    "that phase's GPU inputs")}
+    # device-dependency variant: phases ordered on the device (Runtime::fence), one host wait per step
+    lib.gb_config3_fenced.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    for name, dt in (("config3_attention_f32_fenced", 0), ("config3_attention_bf16_fenced", 4)):
+        lib.gb_config3_fenced(local, dt, 20, out)
+        res[name] = {
+            "workload": "config 3 with the 4 phases ordered on the device by Runtime::fence() (tasks of a phase "
+                        "wait on the device's processed count for the previous phase) and one host wait per step",
+            "step_us": out[0], "tasks_per_s": out[1], "gflops": out[2], "failed_tasks": int(out[3]),
+            "max_rel_err": out[4],
+            "parity": parity_dict(list(out[9:14]), "all 32 heads x 4 phases of the last step vs the oracle on "
+                                                   "that phase's GPU inputs")}
     lib.gb_config4(local, 1_000_000, out)
     res["config4_hot_swap"] = {
         "workload": "1,000,000 fp32 4096-element tasks alternating builtin add and injected scale_add(1.5,-0.25); "
@@ -326,6 +337,16 @@ def run_configs(lib, local: int, tasks2: int, tasks5: int) -> dict:
         "window_rows_checked": int(out[6]), "rows_not_one_variant": int(out[7]),
         "old_rows_past_window": int(out[8]), "failed_tasks": int(out[9]), "canary_hits": int(out[10]),
         "old_rows": int(out[11]), "new_rows": int(out[12])}
+    lib.gb_swap_latency.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.gb_swap_latency(local, 200_000, 16, out)
+    res["config4_swap_latency"] = {
+        "workload": "200,000 fp32 4096-element tasks alternating add and injected scale_add, re-injected 16 times "
+                    "with the ring busy; device trace on",
+        "entry_to_first_new_dispatch_us_p50": out[0], "entry_to_first_new_dispatch_us_max": out[1],
+        "call_return_to_first_new_dispatch_us_p50": out[2], "inject_call_us_p50": out[3],
+        "swaps_measured": int(out[4]), "old_version_dispatches_after_return_max": int(out[5]),
+        "stream_tasks_per_s": out[6],
+        "clock": "device dequeue stamps converted to the host steady clock (ping-pong calibration, +-1 us)"}
     lib.gb_native.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.gb_native(local, 200_000, out)
     res["config4_native_promotion"] = {

@@ -109,6 +109,13 @@ enum gpuos_op_kind {
 #define GPUOS_FLAG_FUSED_COMPOSITE 0x1u
 #define GPUOS_FLAG_SHUTDOWN 0x2u
 #define GPUOS_FLAG_UNCAPPED 0x4u /* matmul/vecmat without the 256 cap (inline path, runtime.hpp:589-594) */
+/* Device-side ordering (extension; the reference has no inter-task ordering,
+ * runtime.hpp:7-9): the task is handed to an executor only after the device's
+ * processed count (gpuos_stats.processed) reaches the target carried in
+ * gpuos_task.enqueue_ns (gpuos_dense_task.wait_target), i.e. after every task
+ * committed before the fence that set the target has completed.  Such tasks
+ * carry no enqueue stamp in the trace. */
+#define GPUOS_FLAG_AFTER 0x8u
 /* A GPUOS_FLAG_FUSED_COMPOSITE task (op id GPUOS_COMPOSITE_OP_ID) carries, in
  * scalars[0], the bits of the device address of its fused program (see
  * gpuos_program_upload) and, in scalars[1], the bits of the device address of
@@ -325,6 +332,7 @@ typedef struct gpuos_dense_task {
   int32_t extents[GPUOS_MAX_RANK];
   uint64_t addr[1 + GPUOS_MAX_INPUTS]; /* [0] = output */
   double scalar0;
+  uint64_t wait_target; /* GPUOS_FLAG_AFTER: processed count to wait for */
 } gpuos_dense_task;
 int gpuos_ring_submit_dense(gpuos_dev* dev, const gpuos_dense_task* task);
 

@@ -933,7 +933,8 @@ int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
     for (uint32_t i = 1; i < gdev::kSlotWords; ++i) w[i] = src[i];
     w[6] = gdev::kFmtExtended;  // gpuos_task.aux is reserved (0)
   }
-  if (d->shadow.trace_on) w[5] = __rdtsc();  // enqueue stamp, converted at trace export
+  // enqueue stamp, converted at trace export (an ordered task's word 5 is its wait target)
+  if (d->shadow.trace_on && !(task->flags & GPUOS_FLAG_AFTER)) w[5] = __rdtsc();
   uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (pos & d->mask) * gdev::kRingSlot);
   uint64_t h = gdev::ring_term(pos + 1, 0);
   for (uint32_t i = 1; i < gdev::kSlotWords; ++i) {
@@ -959,7 +960,7 @@ int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
          ((uint64_t)t->n_scalars << 56);
   w[3] = t->size;
   w[4] = t->done_cell;
-  w[5] = d->shadow.trace_on ? __rdtsc() : 0;
+  w[5] = (t->flags & GPUOS_FLAG_AFTER) ? t->wait_target : (d->shadow.trace_on ? __rdtsc() : 0);
   w[6] = gdev::kFmtCompact | ((uint64_t)t->dtype << 8) | ((uint64_t)t->rank << 16);
   w[8] = (uint64_t)(uint32_t)t->extents[0] | ((uint64_t)(uint32_t)t->extents[1] << 32);
   w[9] = (uint64_t)(uint32_t)t->extents[2] | ((uint64_t)(uint32_t)t->extents[3] << 32);

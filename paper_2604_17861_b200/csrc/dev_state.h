@@ -24,7 +24,7 @@ constexpr uint32_t kJitKindBase = 96;
 constexpr uint32_t kJitSlots = 32;
 constexpr uint32_t kTaskBytes = 384;
 constexpr uint32_t kCtlBytes = 128;     // per-task control block (standalone kernels)
-constexpr uint32_t kHeaderBytes = 7168;  // worker: task buffers, control blocks, counters, entry cache
+constexpr uint32_t kHeaderBytes = 8192;  // worker: task buffers, control blocks, counters, entry cache
 constexpr uint32_t kScratchBytes = 91 * 1024;
 constexpr uint32_t kLaunchCounters = 1u << 16;
 

@@ -244,6 +244,147 @@ __device__ __forceinline__ double nan_skip_max(double a, double b) {
   return a < b ? b : a;
 }
 
+// Batched-head sdpa: the q rows and the scores of up to kSdpaHB heads sit in
+// shared memory; each weight e_i / denom is formed once per key instead of
+// once per (key, column); the output columns of every head in the batch
+// accumulate together, two ascending-key chains per thread with eight keys
+// of v in flight.  Operands are held in their storage type until use (a
+// double per element in flight spilled the unrolled loops to local memory).
+// Every value is computed in the reference's order (ascending j per score,
+// ascending i per output column, ops.hpp:441-498).
+constexpr int kSdpaHB = 8;
+#ifndef GPUOS_SDPA_VU
+#define GPUOS_SDPA_VU 4
+#endif
+constexpr int kSdpaVU = GPUOS_SDPA_VU;  // keys of v in flight per round (pass 3)
+#ifndef GPUOS_SDPA_KU
+#define GPUOS_SDPA_KU 8
+#endif
+constexpr int kSdpaKU = GPUOS_SDPA_KU;  // key elements in flight per round (pass 1)
+__device__ __forceinline__ int sdpa_heads_per_batch(const Ctx* c, int d, int tl) {
+  const int nw = c->nthreads >> 5;
+  if (d > 256 || nw > 8 || d <= 0) return 0;
+  const int fixed = 8 * kSdpaHB + 2 * kSdpaHB + kSdpaHB * d;  // doubles: red, stats, q rows
+  const int avail = c->smem_bytes / 8 - fixed;
+  int hb = kSdpaHB;
+  if (avail / tl < hb) hb = avail / tl;
+  if ((2 * c->nthreads) / d < hb) hb = (2 * c->nthreads) / d;
+  return hb;
+}
+template <int DT>
+__device__ __noinline__ void sdpa_batched(const gpuos_task* t, const Ctx* c, int hb, int64_t hlo, int64_t hhi,
+                                          double scale) {
+  typedef typename DT_<DT>::T T;
+  const gpuos_view& out = t->views[0];
+  const gpuos_view& q = t->views[1];
+  const gpuos_view& kk = t->views[2];
+  const gpuos_view& vv = t->views[3];
+  const int d = q.extents[1], tl = kk.extents[1];
+  const bool exact = exact_products(DT);
+  const int nw = c->nthreads >> 5;
+  double* red = (double*)c->smem;
+  double* stat = red + 8 * kSdpaHB;  // [0, kSdpaHB): max, [kSdpaHB, 2 kSdpaHB): denominator
+  double* qs = stat + 2 * kSdpaHB;
+  double* sc = qs + kSdpaHB * d;
+  const T* qp = (const T*)q.addr;
+  const T* kp = (const T*)kk.addr;
+  const T* vp = (const T*)vv.addr;
+  const int64_t ks0 = kk.strides[0], ks1 = kk.strides[1], ks2 = kk.strides[2];
+  for (int64_t h0 = hlo; h0 < hhi; h0 += hb) {
+    const int nb = (int)((hhi - h0) < hb ? (hhi - h0) : hb);
+    for (int e = c->tid; e < nb * d; e += c->nthreads) {
+      const int hh = e / d, j = e - hh * d;
+      qs[e] = DT_<DT>::gload(qp + (h0 + hh) * q.strides[0] + (int64_t)j * q.strides[1]);
+    }
+    group_sync(c);
+    // pass 1: scores and per-head max; kSdpaKU key elements in flight per round
+#pragma unroll 1
+    for (int hh = 0; hh < nb; ++hh) {
+      const T* kb = kp + (h0 + hh) * ks0;
+      const double* qr = qs + hh * d;
+      double mx = -INFINITY;
+      for (int i = c->tid; i < tl; i += c->nthreads) {
+        const T* kr = kb + (int64_t)i * ks1;
+        double dot = 0.0;
+        for (int j0 = 0; j0 < d; j0 += kSdpaKU) {
+          T kv[kSdpaKU];
+#pragma unroll
+          for (int u = 0; u < kSdpaKU; ++u)
+            if (j0 + u < d) kv[u] = __ldcg(kr + (int64_t)(j0 + u) * ks2);
+#pragma unroll
+          for (int u = 0; u < kSdpaKU; ++u)
+            if (j0 + u < d) dot = mac(dot, qr[j0 + u], DT_<DT>::load(&kv[u]), exact);
+        }
+        const double sv = __dmul_rn(scale, dot);
+        sc[hh * tl + i] = sv;
+        mx = nan_skip_max(mx, sv);
+      }
+      for (int o = 16; o > 0; o >>= 1) mx = nan_skip_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((c->tid & 31) == 0) red[(c->tid >> 5) * kSdpaHB + hh] = mx;
+    }
+    group_sync(c);
+    if (c->tid < nb) {
+      double mx = -INFINITY;
+      for (int w = 0; w < nw; ++w) mx = nan_skip_max(mx, red[w * kSdpaHB + c->tid]);
+      stat[c->tid] = mx;
+    }
+    group_sync(c);
+    // pass 2: e_i = exp(s_i - max) and the per-head denominators
+#pragma unroll 1
+    for (int hh = 0; hh < nb; ++hh) {
+      const double mx = stat[hh];
+      double sum = 0.0;
+      for (int i = c->tid; i < tl; i += c->nthreads) {
+        const double ev = exp(__dsub_rn(sc[hh * tl + i], mx));
+        sc[hh * tl + i] = ev;
+        sum += ev;
+      }
+      sum = warp_sum(sum);
+      if ((c->tid & 31) == 0) red[(c->tid >> 5) * kSdpaHB + hh] = sum;
+    }
+    group_sync(c);
+    if (c->tid < nb) {
+      double sum = 0.0;
+      for (int w = 0; w < nw; ++w) sum += red[w * kSdpaHB + c->tid];
+      stat[kSdpaHB + c->tid] = sum;
+    }
+    group_sync(c);
+    // weights w_i = e_i / denom, once per key
+    for (int e = c->tid; e < nb * tl; e += c->nthreads) sc[e] = __ddiv_rn(sc[e], stat[kSdpaHB + e / tl]);
+    group_sync(c);
+    // pass 3: out[hh][j] = sum_i w_i * v[i][j], ascending i
+    int ph[2], pj[2];
+    double acc[2] = {0.0, 0.0};
+    const T* vb[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int pidx = c->tid + r * c->nthreads;
+      ph[r] = pidx < nb * d ? pidx / d : -1;
+      pj[r] = pidx < nb * d ? pidx - ph[r] * d : 0;
+      vb[r] = vp + (ph[r] >= 0 ? (h0 + ph[r]) * vv.strides[0] + (int64_t)pj[r] * vv.strides[2] : 0);
+    }
+    const int64_t vstep = vv.strides[1];
+    for (int i0 = 0; i0 < tl; i0 += kSdpaVU) {
+      T vr[kSdpaVU][2];
+#pragma unroll
+      for (int u = 0; u < kSdpaVU; ++u)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          if (ph[r] >= 0 && i0 + u < tl) vr[u][r] = __ldcg(vb[r] + (int64_t)(i0 + u) * vstep);
+#pragma unroll
+      for (int u = 0; u < kSdpaVU; ++u)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          if (ph[r] >= 0 && i0 + u < tl)
+            acc[r] = __dadd_rn(acc[r], __dmul_rn(sc[ph[r] * tl + i0 + u], DT_<DT>::load(&vr[u][r])));
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (ph[r] >= 0) DT_<DT>::store((T*)out.addr + (h0 + ph[r]) * out.strides[0] + (int64_t)pj[r] * out.strides[1], acc[r]);
+    group_sync(c);
+  }
+}
+
 __device__ __noinline__ int op_sdpa(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 3) return GPUOS_ARITY_ERROR;
   const gpuos_view& out = t->views[0];
@@ -269,106 +410,15 @@ __device__ __noinline__ int op_sdpa(const gpuos_task* t, const Ctx* c) {
   const char* kp = (const char*)kk.addr;
   const char* vp = (const char*)vv.addr;
   // Batched heads (decode attention: a few heads, d <= 256, contexts whose
-  // scores fit in scratch): the q rows and the scores of up to kHB heads sit in
-  // shared memory, each weight e_i / denom is formed once per key instead of
-  // once per (key, column), and the output columns of every head in the batch
-  // accumulate at once -- each thread carries up to four independent
-  // ascending-key chains.  Every value is computed in the reference's order
-  // (ascending j per score, ascending i per output column).
+  // scores fit in scratch): see sdpa_batched.
   {
-    constexpr int kHB = 8;
-    const int nw = c->nthreads >> 5;
-    const int fixed = 8 * kHB + 2 * kHB + kHB * d;  // doubles: red, stats, q rows
-    const int avail = c->smem_bytes / 8 - fixed;
-    int hb = kHB;
-    if (avail / tl < hb) hb = avail / tl;
-    if ((4 * c->nthreads) / d < hb) hb = (4 * c->nthreads) / d;
-    if (d <= 256 && nw <= 8 && hb >= 1) {
-      double* red = (double*)c->smem;
-      double* stat = red + 8 * kHB;  // [0, kHB): max, [kHB, 2 kHB): denominator
-      double* qs = stat + 2 * kHB;
-      double* sc = qs + kHB * d;
-      for (int64_t h0 = hlo; h0 < hhi; h0 += hb) {
-        const int nb = (int)((hhi - h0) < hb ? (hhi - h0) : hb);
-        for (int e = c->tid; e < nb * d; e += c->nthreads) {
-          const int hh = e / d, j = e - hh * d;
-          qs[e] = load_any(dt, qp, (h0 + hh) * q.strides[0] + (int64_t)j * q.strides[1]);
-        }
-        group_sync(c);
-        // pass 1: scores and per-head max
-#pragma unroll 1
-        for (int hh = 0; hh < nb; ++hh) {
-          const int64_t kb = (h0 + hh) * kk.strides[0];
-          const double* qr = qs + hh * d;
-          double mx = -INFINITY;
-          for (int i = c->tid; i < tl; i += c->nthreads) {
-            const char* kr = kp;
-            const int64_t rb = kb + (int64_t)i * kk.strides[1];
-            double dot = 0.0;
-            for (int j = 0; j < d; ++j) dot = mac(dot, qr[j], load_any(dt, kr, rb + (int64_t)j * kk.strides[2]), exact);
-            const double sv = __dmul_rn(scale, dot);
-            sc[hh * tl + i] = sv;
-            mx = nan_skip_max(mx, sv);
-          }
-          for (int o = 16; o > 0; o >>= 1) mx = nan_skip_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          if ((c->tid & 31) == 0) red[(c->tid >> 5) * kHB + hh] = mx;
-        }
-        group_sync(c);
-        if (c->tid < nb) {
-          double mx = -INFINITY;
-          for (int w = 0; w < nw; ++w) mx = nan_skip_max(mx, red[w * kHB + c->tid]);
-          stat[c->tid] = mx;
-        }
-        group_sync(c);
-        // pass 2: e_i = exp(s_i - max) and the per-head denominators
-#pragma unroll 1
-        for (int hh = 0; hh < nb; ++hh) {
-          const double mx = stat[hh];
-          double sum = 0.0;
-          for (int i = c->tid; i < tl; i += c->nthreads) {
-            const double ev = exp(__dsub_rn(sc[hh * tl + i], mx));
-            sc[hh * tl + i] = ev;
-            sum += ev;
-          }
-          sum = warp_sum(sum);
-          if ((c->tid & 31) == 0) red[(c->tid >> 5) * kHB + hh] = sum;
-        }
-        group_sync(c);
-        if (c->tid < nb) {
-          double sum = 0.0;
-          for (int w = 0; w < nw; ++w) sum += red[w * kHB + c->tid];
-          stat[kHB + c->tid] = sum;
-        }
-        group_sync(c);
-        // weights w_i = e_i / denom, once per key
-        for (int e = c->tid; e < nb * tl; e += c->nthreads) {
-          const int hh = e / tl;
-          sc[e] = __ddiv_rn(sc[e], stat[kHB + hh]);
-        }
-        group_sync(c);
-        // pass 3: out[hh][j] = sum_i w_i * v[i][j], ascending i, four chains per thread
-        int ph[4], pj[4];
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        const char* vb[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int pidx = c->tid + r * c->nthreads;
-          ph[r] = pidx < nb * d ? pidx / d : -1;
-          pj[r] = pidx < nb * d ? pidx - ph[r] * d : 0;
-          vb[r] = vp + (ph[r] >= 0 ? ((h0 + ph[r]) * vv.strides[0] + (int64_t)pj[r] * vv.strides[2]) * dtype_width(dt) : 0);
-        }
-        const int64_t vstep = vv.strides[1];
-        for (int i = 0; i < tl; ++i) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (ph[r] >= 0)
-              acc[r] = __dadd_rn(acc[r], __dmul_rn(sc[ph[r] * tl + i], load_any(dt, vb[r], (int64_t)i * vstep)));
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (ph[r] >= 0)
-            store_any(dt, (char*)out.addr, (h0 + ph[r]) * out.strides[0] + (int64_t)pj[r] * out.strides[1], acc[r]);
-        group_sync(c);
+    const int hb = sdpa_heads_per_batch(c, d, tl);
+    if (hb >= 1) {
+      switch (dt) {
+        case GPUOS_F32: sdpa_batched<GPUOS_F32>(t, c, hb, hlo, hhi, scale); break;
+        case GPUOS_F64: sdpa_batched<GPUOS_F64>(t, c, hb, hlo, hhi, scale); break;
+        case GPUOS_F16: sdpa_batched<GPUOS_F16>(t, c, hb, hlo, hhi, scale); break;
+        default: sdpa_batched<GPUOS_BF16>(t, c, hb, hlo, hhi, scale); break;
       }
       return GPUOS_OK;
     }

@@ -20,7 +20,7 @@
 //   * the executor group calls the body through the device jump table; the
 //     completer warp posts the completion word with a system-scope store
 //     after a gpu-scope release fence, and the per-worker processed count.
-#ifdef GPUOS_LAT_STAMPS
+#if defined(GPUOS_LAT_STAMPS) || defined(GPUOS_FETCH_PROF)
 #include <cstdio>
 #endif
 #include "dev_common.cuh"
@@ -71,7 +71,7 @@ struct SharedCtl {
   uint32_t plan;  // kPlanDenseSame etc. (dev_common.cuh)
   uint16_t part, nparts;  // this buffer's share of its task (both groups run one task when idle)
   uint32_t partial;       // 1: not the task's last part -- the completer posts nothing
-  uint32_t pad;
+  uint32_t compact;       // 1: the descriptor is still the raw compact slot in braw[b] (executors expand it)
 };
 
 constexpr uint32_t kCtlStride = 112;
@@ -148,6 +148,7 @@ struct WorkerHeader {
   gpuos_task task[kBufs];
   SharedCtl ctl[kBufs];
   uint64_t raw[kMaxBatch][kSlotWords];  // slots as read, before expansion
+  uint64_t braw[kBufs][kSlotWords];     // compact slot of buffer b, expanded by its executor group
   uint64_t done;                        // tasks completed by this CTA (all generations)
   uint64_t claimed;                     // tickets claimed by this CTA (all generations)
   uint64_t mbar[kGroups];               // per-group tensor-core completion barriers
@@ -168,6 +169,31 @@ static_assert(sizeof(WorkerHeader) <= kHeaderBytes, "worker header overflows");
 #define LAT_STAMP(i) (H->dbg[i] = clock64())
 #else
 #define LAT_STAMP(i) ((void)0)
+#endif
+// Fetcher hand-off profile (debug builds, make fetch-prof): lane 0 sums the
+// clock64 cycles of each hand-off segment; CTAs 0..3 print the means at exit.
+#ifdef GPUOS_FETCH_PROF
+#define FPROF_DECL long long fp_t = 0, fp_sum[6] = {0, 0, 0, 0, 0, 0}, fp_n = 0;
+#define FPROF_MARK(i)                   \
+  do {                                  \
+    if (lane == 0) {                    \
+      const long long now_ = clock64(); \
+      if ((i) > 0) fp_sum[(i) - 1] += now_ - fp_t; \
+      fp_t = now_;                      \
+    }                                   \
+  } while (0)
+#define FPROF_COUNT() (fp_n += (lane == 0))
+#define FPROF_PRINT()                                                                                             \
+  do {                                                                                                            \
+    if (lane == 0 && w < 4 && fp_n)                                                                               \
+      printf("FPROF cta %u tasks %lld cycles/task: buffer %lld expand %lld slot+ctl %lld resolve %lld arrive %lld\n", \
+             w, fp_n, fp_sum[0] / fp_n, fp_sum[1] / fp_n, fp_sum[2] / fp_n, fp_sum[3] / fp_n, fp_sum[4] / fp_n);   \
+  } while (0)
+#else
+#define FPROF_DECL
+#define FPROF_MARK(i) ((void)0)
+#define FPROF_COUNT() ((void)0)
+#define FPROF_PRINT() ((void)0)
 #endif
 
 // Barrier ids must be immediates where possible (a register id makes ptxas
@@ -469,6 +495,8 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
   uint64_t pre_pos = 0;  // lane 0
   uint32_t pre_nb = 0;   // lane 0
   bool pre = false;      // warp-uniform
+  FPROF_DECL
+  uint32_t tr_last = 0;  // trace_on as last sampled: phase stamps only when tracing
   for (;;) {
     // ---- claim a batch ----
     uint64_t pos = 0;
@@ -488,7 +516,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
     pos = shfl64(pos, 0);
     nb = __shfl_sync(0xffffffffu, nb, 0);
     uint32_t j = 0;  // next slot of the batch to hand over
-    const uint64_t t_ticket = globaltimer();
+    const uint64_t t_ticket = tr_last ? globaltimer() : 0;
     uint32_t spins = 0, expn = 0;
     while (j < nb) {
       // One round of loads, issued back to back: the slots (near tickets
@@ -517,6 +545,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
       if (lane == 0 && tail > h) atomicMax((unsigned long long*)&S->hint, (unsigned long long)tail);
       hint_seen = tail > h ? tail : h;
       if (pos + j > sp) {
+        FPROF_PRINT();
         if (lane == 0) {
           quiesce(K, w);
           F.my_epoch = kQuiescent;
@@ -541,7 +570,9 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
         while (ready < (uint32_t)kMaxBatch && (vb >> (8 * ready)) & 1u) ++ready;
         if (ready == 0 && tb != 0 && lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
         if (ready > 0) {
-          const uint64_t t_seen = globaltimer();
+          const uint32_t tr0 = (uint32_t)shfl64(aux, 3);
+          tr_last = tr0;
+          const uint64_t t_seen = tr0 ? globaltimer() : 0;
           if (lane == 0) LAT_STAMP(0);
           // No acquire fence: executors read task operands with L2 loads only
           // (coherence rule, dev_common.cuh), issued after this read returned
@@ -568,23 +599,50 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
           for (uint32_t i = 0; i < ready; ++i) {
             const uint64_t spos = pos + j;
             const uint64_t* raw = H->raw[i];
+            FPROF_MARK(0);
             const int b = next_buffer(H, F);
+            FPROF_MARK(1);
             gpuos_task* task = &H->task[b];
             SharedCtl* ctl = &H->ctl[b];
             const bool compact = (raw[6] & 0xff) == kFmtCompact;
+            // fields the fetcher itself needs, from the raw compact slot
+            uint32_t op_id, flags;
+            uint64_t tsize, scalar0;
             if (compact) {
-              expand_compact(raw, task, lane);
-
+              // hand the raw slot over: the executor group expands it (24 of
+              // its threads, at wake) -- off the fetcher's per-task path
+              if (lane < 8) reinterpret_cast<uint4*>(H->braw[b])[lane] = reinterpret_cast<const uint4*>(raw)[lane];
+              op_id = (uint32_t)raw[2];
+              flags = (uint32_t)(raw[2] >> 32) & 0xffffu;
+              tsize = raw[3];
+              scalar0 = raw[15];
             } else {
               if (lane < 8) reinterpret_cast<uint4*>(task)[lane] = reinterpret_cast<const uint4*>(raw)[lane];
               __syncwarp();
               fetch_ext(S, K, spos, task, lane);
             }
             __syncwarp();
+            if (!compact) {
+              op_id = task->op_id;
+              flags = task->flags;
+              tsize = task->size;
+              scalar0 = (uint64_t)__double_as_longlong(task->scalars[0]);
+            }
+            FPROF_MARK(2);
             if (lane == 0) LAT_STAMP(1);
             const uint32_t plan = compact ? kPlanDenseSame : plan_task_warp(task, lane);
             bool shutdown = false;
             if (lane == 0) {
+              if (flags & GPUOS_FLAG_AFTER) {
+                // device-side ordering: every task committed before the fence
+                // must have completed (processed is bumped after the
+                // completer's release fence, so their outputs are in L2)
+                const uint64_t target = compact ? raw[5] : task->enqueue_ns;
+                for (uint32_t ns = 32; ld_relaxed_gpu(&S->processed) < target;) {
+                  __nanosleep(ns);
+                  if (ns < 1024) ns <<= 1;
+                }
+              }
               // free the slot for the producer's next lap (queue.hpp:248)
               st_relaxed_sys((uint64_t*)(K.ring + (spos & K.mask) * kRingSlot), spos + K.cap);
               const uint64_t claimed = ++H->claimed;
@@ -596,8 +654,10 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
               ctl->yield_every = ye;
               ctl->trace_on = tr;
               ctl->plan = plan;
+              ctl->compact = compact ? 1u : 0u;
               LAT_STAMP(2);
-              if (task->flags & GPUOS_FLAG_SHUTDOWN) {
+              FPROF_MARK(3);
+              if (flags & GPUOS_FLAG_SHUTDOWN) {
                 atomicMin((unsigned long long*)&S->stop_pos, (unsigned long long)spos);
                 quiesce(K, w);
                 F.my_epoch = kQuiescent;
@@ -606,18 +666,19 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
               } else {
                 if (ver != F.my_epoch) ver = stable_snapshot(S, K, w, ver);
                 F.my_epoch = ver;
-                resolve(S, K, w, H, task->op_id, ver, F.my_epoch, ctl);
-                if ((task->flags & GPUOS_FLAG_FUSED_COMPOSITE) && ctl->code == GPUOS_OK) {
+                resolve(S, K, w, H, op_id, ver, F.my_epoch, ctl);
+                if ((flags & GPUOS_FLAG_FUSED_COMPOSITE) && ctl->code == GPUOS_OK) {
                   // fused elementwise chain (runtime.hpp:912-933): the entry at
                   // the composite id gates it; the program rides in scalars[0]
                   ctl->kind = GPUOS_KIND_PROGRAM;
-                  ctl->aux = (uint64_t)__double_as_longlong(task->scalars[0]);
+                  ctl->aux = scalar0;
                 }
                 ctl->version = ver;
                 LAT_STAMP(3);
-                ctl->t_deq = globaltimer();
+                ctl->t_deq = tr ? globaltimer() : 0;
               }
             }
+            FPROF_MARK(4);
             shutdown = __shfl_sync(0xffffffffu, shutdown, 0);
             // Idle split: with nothing else published, a task large enough to
             // split runs on both executor groups -- this buffer takes part 0
@@ -625,7 +686,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             // completer retires buffers in order, so the task completes once,
             // after both halves.
             const bool split = !shutdown && ready == 1 && nb == 1 && hint_seen <= spos + 1 &&
-                               task->size >= kSplitMin;
+                               tsize >= kSplitMin;
             if (lane == 0) {
               ctl->part = 0;
               ctl->nparts = split ? 2 : 1;
@@ -634,11 +695,17 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             __syncwarp();
             if (lane == 0) LAT_STAMP(4);
             buf_arrive<kBarFull, kFullCount>(b);
+            FPROF_MARK(5);
+            FPROF_COUNT();
             ++F.k;
             ++j;
             if (split) {
               const int b2 = next_buffer(H, F);
-              if (lane < 24) reinterpret_cast<uint4*>(&H->task[b2])[lane] = reinterpret_cast<const uint4*>(task)[lane];
+              if (compact) {
+                if (lane < 8) reinterpret_cast<uint4*>(H->braw[b2])[lane] = reinterpret_cast<const uint4*>(H->braw[b])[lane];
+              } else if (lane < 24) {
+                reinterpret_cast<uint4*>(&H->task[b2])[lane] = reinterpret_cast<const uint4*>(task)[lane];
+              }
               if (lane < (int)(sizeof(SharedCtl) / 8))
                 reinterpret_cast<uint64_t*>(&H->ctl[b2])[lane] = reinterpret_cast<const uint64_t*>(ctl)[lane];
               __syncwarp();
@@ -652,6 +719,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             }
             if (shutdown) {
               // the sentinel's buffer carried the first exit marker
+              FPROF_PRINT();
               fetcher_exit(K, w, H, F, lane, true);
               return;
             }
@@ -716,7 +784,7 @@ counted:
     r->seq = task->seq;
     r->op_id = task->op_id;
     r->worker = w;
-    r->enqueue_ns = task->enqueue_ns;
+    r->enqueue_ns = (task->flags & GPUOS_FLAG_AFTER) ? 0 : task->enqueue_ns;
     r->dequeue_gt = ctl->t_deq;
     r->exec_ns = t_end > ctl->t_deq ? t_end - ctl->t_deq : 1;
     r->version = ctl->version;
@@ -872,7 +940,12 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
       if (warp == 1) tmem_dealloc(H->tmem_base, kTmemCols);
       return;
     }
-    const uint64_t t_wake = globaltimer();
+    if (ctl->compact) {
+      // the fetcher handed over the raw compact slot: 24 threads expand it
+      if (ctx.tid < 24) expand_compact(H->braw[b], task, ctx.tid);
+      group_sync(&ctx);
+    }
+    const uint64_t t_wake = ctl->trace_on ? globaltimer() : 0;
     if (ctx.tid == 0) LAT_STAMP(5);
     int code = ctl->code;
     if (code == GPUOS_OK) {
@@ -913,7 +986,7 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
     if (ctx.tid == 0) {
       ctl->code = code;
       ctl->t_fenced = t_wake;
-      ctl->t_end = globaltimer();
+      ctl->t_end = ctl->trace_on ? globaltimer() : 0;
       mbar_arrive1(&H->done_bar[b]);
     }
   }

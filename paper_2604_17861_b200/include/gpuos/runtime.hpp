@@ -695,9 +695,20 @@ class Runtime {
     if (!chain_.empty()) flush_chain();  // runtime.hpp:392-395
     return h.wait();
   }
+  /// Device-side ordering (extension: the reference orders tasks only through
+  /// host waits, runtime.hpp:7-9).  Every task submitted after fence() starts
+  /// only after every task submitted before it has completed; the producer
+  /// does not block -- the worker that claims a later task waits on the
+  /// device's processed count.  Lasts until the next fence() or wait_all().
+  void fence() {
+    if (!chain_.empty()) flush_chain();
+    fence_target_ = committed_tasks_;
+    fence_on_ = true;
+  }
   void wait_all() {
     if (!chain_.empty()) flush_chain();
     const int rc = gpuos_ring_wait_processed(dev_, committed_tasks_);
+    if (rc == 0) fence_on_ = false;  // everything before any fence is done
     if (rc == static_cast<int>(ErrorCode::RuntimeStopped) && !stopped_)
       throw Error(ErrorCode::RuntimeStopped, "worker generation stopped with tasks pending");
     if (rc != 0 && rc != static_cast<int>(ErrorCode::RuntimeStopped)) check_abi(rc, "wait_all");
@@ -1120,6 +1131,10 @@ class Runtime {
     t->size = static_cast<uint64_t>(output.numel());
     t->done_cell = cells_->device_addr(cell);
     t->enqueue_ns = 0;
+    if (fence_on_) {  // fence(): wait on the device for the tasks committed before it
+      t->flags |= GPUOS_FLAG_AFTER;
+      t->enqueue_ns = fence_target_;
+    }
     t->aux = 0;
     t->checksum = 0;
     for (size_t i = 0; i < kMaxScalars; ++i) t->scalars[i] = i < scalars.size() ? scalars[i] : 0.0;
@@ -1143,7 +1158,8 @@ class Runtime {
     t.seq = id;
     t.done_cell = cells_->device_addr(cell);
     t.op_id = static_cast<uint32_t>(op_id);
-    t.flags = flags;
+    t.flags = fence_on_ ? static_cast<uint16_t>(flags | GPUOS_FLAG_AFTER) : flags;
+    t.wait_target = fence_target_;
     t.n_inputs = static_cast<uint8_t>(inputs.size());
     t.n_scalars = static_cast<uint8_t>(scalars.size());
     t.dtype = static_cast<uint8_t>(output.dtype);
@@ -1231,6 +1247,9 @@ class Runtime {
   void execute_inline(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
                       std::span<const double> scalars, uint32_t cell, uint64_t id) {
     counters_->inc_inline();
+    // after a fence(), a synchronous inline run must not overtake the ring
+    // tasks committed before the fence
+    if (fence_on_) gpuos_ring_wait_processed(dev_, fence_target_);
     const uint64_t t0 = monotonic_ns();
     ErrorCode code = ErrorCode::Ok;
     if (op_id >= table_->slots()) {
@@ -1298,6 +1317,8 @@ class Runtime {
   bool fusion_on_ = false;
   uint64_t next_id_ = 1;
   uint64_t committed_tasks_ = 0;
+  uint64_t fence_target_ = 0;  // committed_tasks_ at the last fence()
+  bool fence_on_ = false;
   uint64_t next_injected_id_ = kFirstInjectedId;
   std::unordered_map<uint32_t, ModulePtr> modules_by_id_;
   gpuos_inject_stats last_inject_{};

@@ -566,6 +566,67 @@ TEST_CASE("live ring invariants: processed <= head <= tail under load, every tas
   CHECK(s.head == s.tail);
 }
 
+// Extension (the reference orders work only through host waits): fence()
+// makes later tasks wait on the device for every earlier task, so a chain of
+// dependent phases runs back to back with a single host wait at the end.
+TEST_CASE("fence: dependent phases without host waits match the waited sequence") {
+  Runtime rt(small_config(4096, 0));
+  const int n = 1500, len = 4096;
+  auto x = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  auto a = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  auto b = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  auto c = rt.alloc_tensor(DType::F32, {int64_t{n} * len});
+  std::mt19937_64 rng(7);
+  std::vector<double> xv = random_vals(rng, static_cast<size_t>(n) * len, -2.0, 2.0);
+  for (double& v : xv) v = f32(v);  // the values an f32 buffer holds
+  fill(rt, x, xv);
+  auto row = [&](const TensorView& base, int i) {
+    TensorView v = base;
+    v.shape = {len};
+    v.strides = {1};
+    v.offset = int64_t{i} * len;
+    return v;
+  };
+  std::vector<TaskHandle> hs;
+  for (int rep = 0; rep < 3; ++rep) {
+    hs.clear();
+    for (int i = 0; i < n; ++i) hs.push_back(rt.submit(OpKind::Relu, {row(x, i)}, row(a, i)));
+    rt.fence();
+    for (int i = 0; i < n; ++i) hs.push_back(rt.submit(OpKind::Mul, {row(a, i), row(x, i)}, row(b, i)));
+    rt.fence();
+    // extended slots too: a rank-0 broadcast of the previous phase's output
+    for (int i = 0; i < n; ++i) {
+      TensorView s0 = row(b, (i + 1) % n);
+      s0.shape = {};
+      s0.strides = {};
+      hs.push_back(rt.submit(OpKind::Add, {row(b, i), s0}, row(c, i)));
+    }
+    rt.wait_all();
+    uint64_t bad_state = 0;
+    for (const TaskHandle& h : hs) bad_state += h.state() == TaskState::Done ? 0 : 1;
+    CHECK(bad_state == 0);
+    const std::vector<double> got = read_all(rt, c);
+    uint64_t bad = 0;
+    for (int i = 0; i < n; ++i) {
+      const double x1 = xv[static_cast<size_t>((i + 1) % n) * len];
+      const double s0 = f32((x1 < 0 ? 0.0 : x1) * x1);
+      for (int k = 0; k < len; ++k) {
+        const double xi = xv[static_cast<size_t>(i) * len + k];
+        const double ai = xi < 0 ? 0.0 : xi;
+        const double bi = f32(ai * xi);
+        bad += got[static_cast<size_t>(i) * len + k] == f32(bi + s0) ? 0 : 1;
+      }
+    }
+    CHECK(bad == 0);
+    // clear the outputs so the next rep cannot pass on stale values
+    fill(rt, a, std::vector<double>(static_cast<size_t>(n) * len, -7.0));
+    fill(rt, b, std::vector<double>(static_cast<size_t>(n) * len, -7.0));
+    fill(rt, c, std::vector<double>(static_cast<size_t>(n) * len, -7.0));
+  }
+  const CounterSnapshot cs = rt.counters();
+  CHECK(cs.processed == cs.committed);
+}
+
 TEST_CASE("hot swap under load: every row is entirely one variant, no canary hits") {
   Runtime rt(small_config(4096, 0));
   const double pa[2] = {1.5, -0.25};

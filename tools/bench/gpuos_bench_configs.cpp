@@ -176,7 +176,10 @@ Mixed make_mixed(Runtime& rt, int n_tasks, uint64_t seed, int64_t out_cap = 0) {
   int64_t tot[4] = {0, 0, 0, 0};  // unwrapped output cursor per dtype
   std::vector<int64_t> start(plans.size());
   m.calls.reserve(plans.size());
-  std::uniform_int_distribution<int64_t> off(0, kIn - 2 * 65536 - 16);
+  std::uniform_int_distribution<int64_t> off_raw(0, kIn - 2 * 65536 - 16);
+  // GB_FORCE_ALIGN=1 (diagnostics): every view starts 16-byte aligned
+  const bool align16 = std::getenv("GB_FORCE_ALIGN") != nullptr;
+  auto off = [&](std::mt19937_64& r) { return align16 ? off_raw(r) & ~int64_t{7} : off_raw(r); };
   for (size_t pi = 0; pi < plans.size(); ++pi) {
     const Plan& p = plans[pi];
     Gen g;
@@ -190,6 +193,7 @@ Mixed make_mixed(Runtime& rt, int n_tasks, uint64_t seed, int64_t out_cap = 0) {
     const TensorView& OUT = m.outA[p.dt];
     const int64_t R = p.r, Cc = p.c, n = p.n;
     const int64_t n_out = g.op == OpKind::ReduceSum ? R : n;
+    if (align16) tot[p.dt] = (tot[p.dt] + 7) & ~int64_t{7};
     int64_t pos = tot[p.dt] % cap[p.dt];
     if (pos + n_out > cap[p.dt]) {  // next lap
       tot[p.dt] += cap[p.dt] - pos;
@@ -438,7 +442,7 @@ int gb_config2(int device, int n_tasks, int steps, double* out) {
 //      [4] max relative error over the checked outputs,
 //      [5..8] median us of the scale / QK^T / softmax / PV phases,
 //      [9..13] parity (put_tally) of the last step: all heads, all phases
-int gb_config3(int device, int dtype, int steps, double* out) {
+static int config3_impl(int device, int dtype, int steps, bool fenced, double* out) {
   const int H = 32, S = 128, D = 64;
   const DType dt = static_cast<DType>(dtype);
   Runtime rt(bench_cfg(device, 4096));
@@ -491,9 +495,13 @@ int gb_config3(int device, int dtype, int steps, double* out) {
     if (s == steps + 1)  // the verified (last) step can only pass on its own outputs
       for (const TensorView* t : {&Qs, &Sc, &P, &O}) rt.pool().fill(t->buffer, 0xff);
     const double t0 = now_ms();
+    if (fenced) hs.clear();
     for (int phase = 0; phase < 4; ++phase) {
       const double tp = now_ms();
-      hs.clear();
+      // device-dependency variant: the phases are ordered on the device by a
+      // fence (Runtime::fence), one host wait per step instead of four
+      if (fenced && phase > 0) rt.fence();
+      if (!fenced) hs.clear();
       for (int h = 0; h < H; ++h) {
         switch (phase) {
           case 0: hs.push_back(rt.submit(OpKind::Mul, {head(Q, h, S, D), sc0}, head(Qs, h, S, D))); break;
@@ -506,11 +514,19 @@ int gb_config3(int device, int dtype, int steps, double* out) {
           default: hs.push_back(rt.submit(OpKind::MatMulSmall, {head(P, h, S, S), head(V, h, S, D)}, head(O, h, S, D)));
         }
       }
+      if (fenced) continue;
       for (const TaskHandle& th : hs) {
         th.wait();
         if (s >= 2) failed += th.state() == TaskState::Failed ? 1 : 0;
       }
       if (s >= 2) phase_us[phase].push_back((now_ms() - tp) * 1e3);
+    }
+    if (fenced) {
+      rt.wait_all();
+      for (const TaskHandle& th : hs)
+        if (s >= 2) failed += th.state() == TaskState::Failed ? 1 : 0;
+      for (int phase = 0; phase < 4; ++phase)
+        if (s >= 2) phase_us[phase].push_back(0.0);
     }
     if (s >= 2) step_us.push_back((now_ms() - t0) * 1e3);
   }
@@ -605,6 +621,13 @@ int gb_config3(int device, int dtype, int steps, double* out) {
 //      [6] checked rows, [7] rows not uniformly one variant, [8] rows with the
 //      old variant after the swap window, [9] failed tasks, [10] canary hits,
 //      [11] old rows, [12] new rows
+int gb_config3(int device, int dtype, int steps, double* out) { return config3_impl(device, dtype, steps, false, out); }
+// Device-dependency variant of config 3 (SURVEY §8(d) "report both"): the
+// four phases are separated by Runtime::fence() instead of host waits.
+int gb_config3_fenced(int device, int dtype, int steps, double* out) {
+  return config3_impl(device, dtype, steps, true, out);
+}
+
 int gb_config4(int device, int n_tasks, double* out) {
   const int64_t E = 4096;
   const int kIn = 8;
@@ -693,6 +716,79 @@ int gb_config4(int device, int n_tasks, double* out) {
   out[10] = static_cast<double>(rt.canary_hits());
   out[11] = static_cast<double>(old_rows);
   out[12] = static_cast<double>(new_rows);
+  return 0;
+}
+
+// Swap latency as SURVEY §8(d) config 4 defines it: inject_operator_at entry
+// -> the first device dispatch of the id under the new table version (the
+// device trace's dequeue stamp, converted to the host clock by the ping-pong
+// calibration, +-1 us), with the ring busy: a stream of 4096-element tasks
+// alternating builtin add and the injected op, re-injected `swaps` times.
+// out: [0] p50 entry->first new dispatch us, [1] max, [2] p50 call-return ->
+//      first new dispatch us, [3] p50 inject call us, [4] swaps measured,
+//      [5] dispatches of the old version after the call returned (max over swaps),
+//      [6] tasks/s of the traced stream
+int gb_swap_latency(int device, int n_tasks, int swaps, double* out) {
+  const int64_t E = 4096;
+  RuntimeConfig cfg = bench_cfg(device, 4096);
+  cfg.telemetry_enabled = true;
+  cfg.trace_capacity = static_cast<size_t>(n_tasks) + 4096;
+  Runtime rt(cfg);
+  const double pa[2] = {1.5, -0.25}, pb[2] = {-2.0, 3.0};
+  const uint32_t id = static_cast<uint32_t>(rt.inject_operator("scale_add", pa));
+  TensorView IN = rt.alloc_tensor(DType::F32, {8 * E});
+  TensorView OUT = rt.alloc_tensor(DType::F32, {1024 * E});
+  rt.wait_all();
+  struct Swap {
+    uint64_t entry, exit, version;
+  };
+  std::vector<Swap> sw;
+  const int every = n_tasks / (swaps + 1);
+  const uint64_t t0 = monotonic_ns();
+  for (int t = 0; t < n_tasks; ++t) {
+    const TensorView in = view_of(IN, static_cast<int64_t>(t % 8) * E, {E}, {1});
+    const TensorView o = view_of(OUT, static_cast<int64_t>(t % 1024) * E, {E}, {1});
+    if (t % 2 == 0) rt.submit(OpKind::Add, {in, in}, o);
+    else rt.submit(static_cast<uint64_t>(id), {in}, o);
+    if (t > 0 && t % every == 0 && static_cast<int>(sw.size()) < swaps) {
+      Swap s;
+      s.entry = monotonic_ns();
+      rt.inject_operator_at(id, "scale_add", (sw.size() % 2 == 0) ? std::span<const double>(pb, 2)
+                                                                  : std::span<const double>(pa, 2));
+      s.exit = monotonic_ns();
+      s.version = rt.table().snapshot_version();
+      sw.push_back(s);
+    }
+  }
+  rt.wait_all();
+  const double secs = static_cast<double>(monotonic_ns() - t0) / 1e9;
+  const std::vector<Tracepoint> tr = rt.trace();
+  std::vector<double> lat_entry, lat_exit, call;
+  uint64_t late_old_max = 0;
+  for (const Swap& s : sw) {
+    uint64_t first = UINT64_MAX, late_old = 0;
+    for (const Tracepoint& p : tr) {
+      if (p.op_id != id) continue;
+      if (p.version >= s.version && p.dequeue_ns >= s.entry && p.dequeue_ns < first) first = p.dequeue_ns;
+      if (p.version < s.version && p.dequeue_ns > s.exit) ++late_old;
+    }
+    if (first == UINT64_MAX) continue;
+    lat_entry.push_back(static_cast<double>(first - s.entry) / 1e3);
+    lat_exit.push_back(static_cast<double>(static_cast<int64_t>(first - s.exit)) / 1e3);
+    call.push_back(static_cast<double>(s.exit - s.entry) / 1e3);
+    late_old_max = std::max(late_old_max, late_old);
+  }
+  auto med = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v.empty() ? -1.0 : v[v.size() / 2];
+  };
+  out[0] = med(lat_entry);
+  out[1] = lat_entry.empty() ? -1.0 : *std::max_element(lat_entry.begin(), lat_entry.end());
+  out[2] = med(lat_exit);
+  out[3] = med(call);
+  out[4] = static_cast<double>(lat_entry.size());
+  out[5] = static_cast<double>(late_old_max);
+  out[6] = n_tasks / secs;
   return 0;
 }
 

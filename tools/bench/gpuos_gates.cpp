@@ -98,6 +98,7 @@ struct Row {
   std::string workload;
   Mode mode;
   uint64_t config = 0, ops = 0, total_ns = 0, checksum = 0, extra = 0, aux = 0, p50 = 0, p99 = 0;
+  std::map<std::string, uint64_t> op_p50;  // per-operator submit -> wait p50 (attention)
 };
 
 // The GPU's workers are SMs, not threads: spec.workers (the reference's host
@@ -222,10 +223,13 @@ std::vector<Row> run_attention(const Spec& spec, Mode m) {
     fill_view(*rt, b, beta);
     fill_view(*rt, kcache, kc0);
     fill_view(*rt, vcache, vc0);
+    std::map<std::string, std::vector<uint64_t>> op_lat;
     auto step = [&](OpKind kind, std::vector<TensorView> inputs, const TensorView& out,
                     std::vector<double> scalars = {}) {
+      const uint64_t t0 = monotonic_ns();
       TaskHandle hd = rt->submit(kind, std::move(inputs), out, std::move(scalars));
       if (rt->wait(hd) != TaskState::Done) ++row.extra;
+      op_lat[op_kind_name(kind)].push_back(monotonic_ns() - t0);
     };
     std::vector<uint64_t> lat;
     const uint64_t w0 = monotonic_ns();
@@ -258,6 +262,13 @@ std::vector<Row> run_attention(const Spec& spec, Mode m) {
     hsh = checksum_view(hsh, *rt, vcache);
     row.checksum = hsh;
     row.aux = static_cast<uint64_t>(prefill + tokens);
+    for (auto& [k, v] : op_lat) row.op_p50[k] = pct(v, 0.5);
+    {  // device-side body time per operator (trace exec_ns)
+      std::map<std::string, std::vector<uint64_t>> ex;
+      for (const Tracepoint& t : rt->trace())
+        if (t.op_id < kNumBuiltinOps) ex[std::string("exec_") + op_kind_name(static_cast<OpKind>(t.op_id))].push_back(t.exec_ns);
+      for (auto& [k, v] : ex) row.op_p50[k] = pct(v, 0.5);
+    }
     row.p50 = pct(lat, 0.5);
     row.p99 = pct(lat, 0.99);
     rows.push_back(row);
@@ -758,12 +769,20 @@ bool gate_attention() {
   std::printf("{\"gate\": \"attention\", \"pass\": %s, \"what\": \"decode attention h=4 d=64, 100 tokens x 7 "
               "dependent ops (rope, 2 mul, kv_append, sdpa, layernorm, add), host waits between ops\", \"rows\": [",
               same ? "true" : "false");
-  for (size_t i = 0; i < p.size(); ++i)
+  for (size_t i = 0; i < p.size(); ++i) {
     std::printf("%s{\"context\": %llu, \"persistent_token_p50_us\": %.2f, \"persistent_token_p99_us\": %.2f, "
-                "\"per_op_launch_token_p50_us\": %.2f, \"speedup_p50\": %.2f, \"checksums_equal\": %s}",
+                "\"per_op_launch_token_p50_us\": %.2f, \"speedup_p50\": %.2f, \"checksums_equal\": %s, "
+                "\"persistent_op_p50_us\": {",
                 i ? ", " : "", (unsigned long long)p[i].config, p[i].p50 / 1e3, p[i].p99 / 1e3, c[i].p50 / 1e3,
                 static_cast<double>(c[i].p50) / static_cast<double>(std::max<uint64_t>(1, p[i].p50)),
                 p[i].checksum == c[i].checksum ? "true" : "false");
+    bool first = true;
+    for (const auto& [k, v] : p[i].op_p50) {
+      std::printf("%s\"%s\": %.2f", first ? "" : ", ", k.c_str(), v / 1e3);
+      first = false;
+    }
+    std::printf("}}");
+  }
   std::printf("]}\n");
   std::fflush(stdout);
   return same;
