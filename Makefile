@@ -11,7 +11,8 @@ CC ?= gcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVEXTRA ?=
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $(NVEXTRA)
-CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -Iinclude -Ipaper_2604_17861_b200/include
+CUDA_HOME ?= /usr/local/cuda
+CXXFLAGS := -std=c++20 -O3 -ffp-contract=off -fPIC -Wall -Wno-unused-function -Iinclude -Ipaper_2604_17861_b200/include -isystem $(CUDA_HOME)/include
 LIBDIR := paper_2604_17861_b200/lib
 CSRC := paper_2604_17861_b200/csrc
 OBJ := build/obj

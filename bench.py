@@ -437,6 +437,7 @@ def main() -> None:
     base_steps = max(1, min(args.steps, 3))
     step(1)  # warm
     b_dev = [step(1)[0] for _ in range(base_steps)]
+    lean_dev = [step(3)[0] for _ in range(base_steps)]  # lean per-op launches (minimal add kernel)
     # queue-depth-1 latency, persistent vs per-op launch
     lat = (C.c_double * 3)()
     lib.gb_latency(h, 0, 10_000, 1_000, lat)
@@ -482,6 +483,7 @@ def main() -> None:
         with open(tp) as f:
             traffic = json.load(f).get("bytes_per_step")
     base_value = N_TASKS / (statistics.median(b_dev) / 1e3)
+    lean_value = N_TASKS / (statistics.median(lean_dev) / 1e3)
     cpu = None
     if not args.no_cpu_baseline:
         r = ref_cpu_baseline(seconds=args.cpu_seconds)
@@ -503,6 +505,10 @@ def main() -> None:
         "host_submit_ns_per_task": 1e6 * statistics.median(sub_ms) / N_TASKS,
         "baseline_per_op_launch": {"value": base_value, "unit": "tasks/s", "p50_launch_sync_us": lp50,
                                    "p99_launch_sync_us": lp99, "speedup": value / (base_value * world)},
+        "baseline_per_op_launch_lean": {
+            "value": lean_value, "unit": "tasks/s", "speedup": value / (lean_value * world),
+            "what": "one cudaLaunchKernel per task of a minimal dense f32 add kernel (4 parameters, no "
+                    "descriptor, no dynamic shared memory, no lock, grid sized to the op), device-timed"},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peaks["source"],
                      "kernel": "gpuos_worker_kernel (per step: 10,000 x 49,152 algorithmic bytes, slowest GPU)"},

@@ -388,6 +388,11 @@ int gpuos_trace_phases(gpuos_dev* dev, gpuos_trace_phase* out, uint64_t cap, uin
  * (execute_inline, runtime.hpp:567-619).  `stream` is a cudaStream_t or NULL
  * for the runtime's side stream.  The body writes task->done_cell. */
 int gpuos_launch_task(gpuos_dev* dev, const gpuos_task* task, void* stream);
+/* Lean per-op baseline (measurement only, not a task path): one launch of a
+ * minimal dense f32 add kernel -- 4 small parameters, no descriptor, no dynamic
+ * shared memory, no table lookup, no lock.  The caller owns the device's
+ * current context; pointers must be 16-byte aligned. */
+int gpuos_launch_lean_add(gpuos_dev* dev, void* out, const void* a, const void* b, int64_t n, void* stream);
 int gpuos_stream_create(gpuos_dev* dev, void** stream);
 int gpuos_stream_sync(gpuos_dev* dev, void* stream);
 int gpuos_stream_destroy(gpuos_dev* dev, void* stream);

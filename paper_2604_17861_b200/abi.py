@@ -105,7 +105,7 @@ EXPORTS = [
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
     "gpuos_ring_wait_processed", "gpuos_dev_debug", "gpuos_table_slots", "gpuos_table_version", "gpuos_table_status",
     "gpuos_table_install_builtin", "gpuos_table_install_program", "gpuos_table_kill",
-    "gpuos_dev_get_stats", "gpuos_trace_enable", "gpuos_trace_snapshot", "gpuos_trace_phases", "gpuos_launch_task",
+    "gpuos_dev_get_stats", "gpuos_trace_enable", "gpuos_trace_snapshot", "gpuos_trace_phases", "gpuos_launch_task", "gpuos_launch_lean_add",
     "gpuos_stream_create", "gpuos_stream_sync", "gpuos_stream_destroy", "gpuos_dev_kernel_stream",
     "gpuos_event_create", "gpuos_event_record", "gpuos_event_sync", "gpuos_event_elapsed_ms",
     "gpuos_event_destroy", "gpuos_host_alloc", "gpuos_copy_async", "gpuos_jit_compile", "gpuos_free",
@@ -173,6 +173,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_trace_snapshot": ([P, C.POINTER(Tracepoint), U64, C.POINTER(U64)], I),
         "gpuos_trace_phases": ([P, C.POINTER(TracePhase), U64, C.POINTER(U64)], I),
         "gpuos_launch_task": ([P, C.POINTER(Task), P], I),
+        "gpuos_launch_lean_add": ([P, P, P, P, C.c_int64, P], I),
         "gpuos_stream_create": ([P, C.POINTER(P)], I),
         "gpuos_stream_sync": ([P, P], I),
         "gpuos_stream_destroy": ([P, P], I),

@@ -1414,6 +1414,14 @@ int gpuos_launch_task(gpuos_dev* d, const gpuos_task* t, void* stream) {
   return GPUOS_OK;
 }
 
+int gpuos_launch_lean_add(gpuos_dev* d, void* out, const void* a, const void* b, int64_t n, void* stream) {
+  if (!d || !out || !a || !b || n < 0 || n >= (int64_t{1} << 31)) return GPUOS_INTERNAL;
+  if ((((uintptr_t)out) | ((uintptr_t)a) | ((uintptr_t)b)) & 15) return GPUOS_INTERNAL;
+  GPUOS_CK(gdev::launch_lean_add((float*)out, (const float*)a, (const float*)b, (int)n,
+                                 stream ? (cudaStream_t)stream : d->side));
+  return GPUOS_OK;
+}
+
 int gpuos_stream_create(gpuos_dev* d, void** stream) {
   if (!d || !stream) return GPUOS_INTERNAL;
   cudaSetDevice(d->device);
@@ -1597,7 +1605,10 @@ int gpuos_jit_compile_object(const char* src, void** obj, size_t* size, uint64_t
   const uint64_t t0 = steady_ns();
   nvrtcProgram prog;
   if (J.create(&prog, src, "gpuos_native_op.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return GPUOS_INTERNAL;
-  // register cap = the image's (-maxrregcount=80 in the Makefile): rdc callees must fit every caller
+  // register cap = the image's (-maxrregcount=80 in the Makefile): rdc callees
+  // must fit every caller.  (A 112-register image -- the product worker's
+  // __maxnreg__ -- measured slower after promotion: 15.7M vs 19.4M native
+  // tasks/s, and 83 vs 3-22 ms module load; profiles/r02_bench_full_v5.json)
   const char* o[] = {"-arch=sm_100a", "-rdc=true", "--fmad=false", "-std=c++17", "-default-device", "--maxrregcount=80",
                      "-DGPUOS_JIT_TU=1", inc_csrc.c_str(), inc_abi.c_str(), inc_cuda.c_str()};
   if (J.compile(prog, (int)(sizeof(o) / sizeof(o[0])), o) != NVRTC_SUCCESS) {

@@ -117,6 +117,7 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
 cudaError_t launch_clock_probe(const uint32_t* flag, uint64_t* out, int rounds, cudaStream_t st);
 // Stream-ordered generation start: claim/hint/stop_pos in one tiny launch
 // (three pageable 8-byte copies cost more stream time than the launch).
+cudaError_t launch_lean_add(float* out, const float* a, const float* b, int n, cudaStream_t st);
 cudaError_t launch_gen_init(DevState* s, uint64_t claim, uint64_t hint, uint64_t stop_pos, cudaStream_t st);
 uint32_t worker_smem_bytes();
 uint32_t worker_threads();

@@ -47,6 +47,30 @@ template <class F>
 struct HasF32<F, decltype((void)F::kF32)> {
   static constexpr bool value = F::kF32;
 };
+// f32 evaluation of add/mul/relu for the 16- and 32-bit float dtypes.  For
+// F16/BF16 the operands widen to f32 exactly, f32 add/mul round once to 24
+// bits, and the narrowing to 11 (f16) or 8 (bf16) bits is then the correctly
+// rounded result of the exact sum/product -- double rounding is innocuous
+// when 24 >= 2q + 2 (q = 11 or 8), the same argument as double -> f32 above;
+// f32 subnormals and overflow map to the 16-bit format's the same way.  So
+// this is bit-identical to the reference's double evaluation narrowed once.
+template <int DT>
+struct F32Eval {
+  static constexpr bool value = DT == GPUOS_F32 || DT == GPUOS_F16 || DT == GPUOS_BF16;
+};
+template <int DT>
+__device__ __forceinline__ float to_f32(typename DT_<DT>::T v) {
+  if constexpr (DT == GPUOS_F16) return __half2float(v);
+  else if constexpr (DT == GPUOS_BF16) return __bfloat162float(v);
+  else return (float)v;
+}
+template <int DT>
+__device__ __forceinline__ typename DT_<DT>::T from_f32(float v) {
+  if constexpr (DT == GPUOS_F16) return __float2half_rn(v);
+  else if constexpr (DT == GPUOS_BF16) return __float2bfloat16_rn(v);
+  else return v;
+}
+
 struct FGelu {
   static constexpr int A = 1;
   // 0.5 * x * (1 + tanh(c * (x + 0.044715 * x * x * x))), c = sqrt(2/pi)  (ops.hpp:79-82)
@@ -102,11 +126,11 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
           T* eo = reinterpret_cast<T*>(&vo);
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            if constexpr (DT == GPUOS_F32 && HasF32<F>::value) {
+            if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
               float x[A];
 #pragma unroll
-              for (int k = 0; k < A; ++k) x[k] = reinterpret_cast<const float*>(ev[k])[j];
-              reinterpret_cast<float*>(eo)[j] = f.f32(x);
+              for (int k = 0; k < A; ++k) x[k] = to_f32<DT>(ev[k][j]);
+              eo[j] = from_f32<DT>(f.f32(x));
             } else {
               double x[A];
 #pragma unroll
@@ -123,9 +147,34 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
   } else if constexpr (!kAligned) {
     // an operand is not 16-byte aligned (views at arbitrary element offsets):
     // element loads, still coalesced across the warp, with UE elements per
-    // thread in flight so a round costs one memory latency, not UE
+    // thread in flight so a round costs one memory latency, not UE.  f32
+    // add/mul/relu stay in f32 registers (bit-identical, see FAdd), which
+    // halves the registers per element in flight.  (A funnel-shifted 16-byte
+    // vector variant -- two aligned blocks per vector, or one block plus a
+    // lane shuffle -- measured slower here: 7.6-8.0M vs 13.8M config-2 tasks/s.)
     int64_t lo, hi;
     part_range(n, c->part, c->nparts, 1, &lo, &hi);
+    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+      constexpr int UE = 16;
+      const int64_t step = (int64_t)c->nthreads * UE;
+      for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
+        float x[UE][A];
+#pragma unroll
+        for (int u = 0; u < UE; ++u) {
+          const int64_t e = e0 + (int64_t)u * c->nthreads;
+          if (e < hi) {
+#pragma unroll
+            for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + e));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UE; ++u) {
+          const int64_t e = e0 + (int64_t)u * c->nthreads;
+          if (e < hi) out[e] = from_f32<DT>(f.f32(x[u]));
+        }
+      }
+      return;
+    }
     constexpr int UE = 8;
     const int64_t step = (int64_t)c->nthreads * UE;
     for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
@@ -171,6 +220,27 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
     int64_t st[1 + A];
 #pragma unroll
     for (int k = 0; k <= A; ++k) st[k] = s.st[k][0];
+    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+      constexpr int U1F = 16;
+      const int64_t stepf = (int64_t)c->nthreads * U1F;
+      for (int64_t e0 = lo + c->tid; e0 < hi; e0 += stepf) {
+        float x[U1F][A];
+#pragma unroll
+        for (int u = 0; u < U1F; ++u) {
+          const int64_t e = e0 + (int64_t)u * c->nthreads;
+          if (e < hi) {
+#pragma unroll
+            for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + e * st[1 + k]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U1F; ++u) {
+          const int64_t e = e0 + (int64_t)u * c->nthreads;
+          if (e < hi) out[e * st[0]] = from_f32<DT>(f.f32(x[u]));
+        }
+      }
+      return;
+    }
     constexpr int U1 = 8;
     const int64_t step = (int64_t)c->nthreads * U1;
     for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
@@ -201,6 +271,95 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
       st1[k] = s.st[k][1];
     }
     const FastDiv fd = s.fd[1];
+    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+      // 32-bit offsets when every operand's span fits (config-2 views do)
+      int64_t span = 0;
+#pragma unroll
+      for (int k = 0; k <= A; ++k) {
+        const int64_t a0 = st0[k] < 0 ? -st0[k] : st0[k], a1 = st1[k] < 0 ? -st1[k] : st1[k];
+        const int64_t sp = a0 * (s.ext[0] - 1) + a1 * (s.ext[1] - 1);
+        span = sp > span ? sp : span;
+      }
+      if (span < ((int64_t)1 << 31)) {
+        int32_t s0[1 + A], s1[1 + A];
+#pragma unroll
+        for (int k = 0; k <= A; ++k) {
+          s0[k] = (int32_t)st0[k];
+          s1[k] = (int32_t)st1[k];
+        }
+        // Transposed inputs (row stride 1, column stride > 1) against a
+        // row-major output: 32x32 tiles per warp through shared memory, so
+        // both the column-major reads and the row-major writes coalesce.
+        bool tr[A];
+        bool any_tr = false;
+#pragma unroll
+        for (int k = 0; k < A; ++k) {
+          tr[k] = s0[1 + k] == 1 && (s1[1 + k] > 1 || s1[1 + k] < -1);
+          any_tr = any_tr || tr[k];
+        }
+        const int nw = c->nthreads >> 5;
+        if (any_tr && s1[0] == 1 && c->smem_bytes >= nw * A * 32 * 33 * 4 && s.ext[0] >= 8) {
+          const int lane = c->tid & 31, warp = c->tid >> 5;
+          const int R = s.ext[0], C = s.ext[1];
+          const int tcols = (C + 31) / 32;
+          const int64_t ntiles = (int64_t)((R + 31) / 32) * tcols;
+          int64_t tlo, thi;
+          part_range(ntiles, c->part, c->nparts, 1, &tlo, &thi);
+          float* tile = reinterpret_cast<float*>(c->smem) + (size_t)warp * A * 32 * 33;
+          for (int64_t tt = tlo + warp; tt < thi; tt += nw) {
+            const int q0 = (int)(tt / tcols) * 32, r0 = (int)(tt % tcols) * 32;
+#pragma unroll
+            for (int k = 0; k < A; ++k) {
+              if (!tr[k]) continue;
+              float v[32];
+              const int q = q0 + lane;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                v[i] = (q < R && r0 + i < C) ? to_f32<DT>(__ldcg(in[k] + (q * s0[1 + k] + (r0 + i) * s1[1 + k]))) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) tile[(k * 32 + i) * 33 + lane] = v[i];
+            }
+            __syncwarp();
+            const int r = r0 + lane;
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              const int q = q0 + i;
+              if (q < R && r < C) {
+                float x[A];
+#pragma unroll
+                for (int k = 0; k < A; ++k)
+                  x[k] = tr[k] ? tile[(k * 32 + lane) * 33 + i] : to_f32<DT>(__ldcg(in[k] + (q * s0[1 + k] + r * s1[1 + k])));
+                out[q * s0[0] + r] = from_f32<DT>(f.f32(x));
+              }
+            }
+            __syncwarp();
+          }
+          return;
+        }
+        constexpr int U2F = 16;
+        const int64_t stepf = (int64_t)c->nthreads * U2F;
+        for (int64_t e0 = lo + c->tid; e0 < hi; e0 += stepf) {
+          float x[U2F][A];
+          int32_t oo[U2F];
+#pragma unroll
+          for (int u = 0; u < U2F; ++u) {
+            const int64_t e = e0 + (int64_t)u * c->nthreads;
+            if (e < hi) {
+              const uint32_t q = fd.div((uint32_t)e), r = (uint32_t)e - q * fd.d;
+              oo[u] = (int32_t)q * s0[0] + (int32_t)r * s1[0];
+#pragma unroll
+              for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + ((int32_t)q * s0[1 + k] + (int32_t)r * s1[1 + k])));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U2F; ++u) {
+            const int64_t e = e0 + (int64_t)u * c->nthreads;
+            if (e < hi) out[oo[u]] = from_f32<DT>(f.f32(x[u]));
+          }
+        }
+        return;
+      }
+    }
     constexpr int U2 = 8;
     const int64_t step = (int64_t)c->nthreads * U2;
     for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {

@@ -335,6 +335,79 @@ __device__ __forceinline__ double lane_sum(const char* ib, int64_t si, int64_t c
   return s;
 }
 
+// Contiguous row (unit stride): a scalar head up to 16-byte alignment, then
+// kSumVec 16-byte vectors per lane in flight, then a scalar tail.  The fp64
+// lane partials are combined by the unit's tree (<= 1 ulp rule, as above).
+constexpr int kSumVec = 4;
+template <int DT>
+__device__ __forceinline__ double lane_sum_vec(const char* ib, int64_t cols, const RowSched& rs) {
+  typedef typename DT_<DT>::T T;
+  constexpr int V = 16 / (int)sizeof(T);
+  const T* p = (const T*)ib;
+  int64_t head = (int64_t)(((16 - ((uintptr_t)p & 15)) & 15) / sizeof(T));
+  if (head > cols) head = cols;
+  const int64_t nv = (cols - head) / V;
+  double s = 0.0;
+  if (rs.lane < head) s += DT_<DT>::gload(p + rs.lane);
+  const uint4* vb = reinterpret_cast<const uint4*>(p + head);
+  for (int64_t i0 = rs.lane; i0 < nv; i0 += (int64_t)rs.width * kSumVec) {
+    uint4 v[kSumVec];
+#pragma unroll
+    for (int u = 0; u < kSumVec; ++u) {
+      const int64_t i = i0 + (int64_t)u * rs.width;
+      v[u] = i < nv ? ld_cg_v4(vb + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kSumVec; ++u)
+#pragma unroll
+      for (int j = 0; j < V; ++j) s += DT_<DT>::load(reinterpret_cast<const T*>(&v[u]) + j);
+  }
+  for (int64_t j = head + nv * V + rs.lane; j < cols; j += rs.width) s += DT_<DT>::gload(p + j);
+  return s;
+}
+
+// Interleaved rows (a transposed 2-D view: row stride 1, element stride >
+// 1): one thread per row walks its elements in order, so a warp's loads are
+// 32 consecutive rows' elements -- coalesced -- and the sum / first-wins scan
+// is the reference's left-to-right order exactly.
+template <int MODE, int DT>
+__device__ __forceinline__ void reduce_rows_by_thread(const gpuos_view& in, const gpuos_view& out, int64_t rows,
+                                                      int64_t cols, const Ctx* c) {
+  typedef typename DT_<DT>::T T;
+  const T* ib = (const T*)in.addr;
+  T* ob = (T*)out.addr;
+  const int64_t si = in.strides[1];
+  int64_t lo, hi;
+  part_range(rows, c->part, c->nparts, 1, &lo, &hi);
+  constexpr int U = 8;
+  for (int64_t r = lo + c->tid; r < hi; r += c->nthreads) {
+    const T* rp = ib + r;  // in.strides[0] == 1
+    double acc = 0.0, best = 0.0;
+    int64_t bi = -1;
+    for (int64_t j0 = 0; j0 < cols; j0 += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = j0 + u < cols ? DT_<DT>::gload(rp + (j0 + u) * si) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (j0 + u >= cols) break;
+        if (MODE == 0) {
+          acc += v[u];
+        } else if (v[u] == v[u] && (bi < 0 || (MODE == 1 ? best < v[u] : v[u] < best))) {
+          best = v[u];
+          bi = j0 + u;
+        }
+      }
+    }
+    double res = acc;
+    if (MODE != 0) {
+      const double x0 = DT_<DT>::gload(rp);
+      res = (x0 != x0 || bi < 0) ? x0 : best;
+    }
+    DT_<DT>::store(ob + r * out.strides[0], res);
+  }
+}
+
 template <int MODE>  // 0 sum, 1 max, 2 min
 __device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
@@ -351,8 +424,50 @@ __device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
   if ((b = bind_code(in)) || (b = bind_code(out))) return b;
   const int dt = out.dtype;
   const int64_t si = in.strides[in.rank - 1];
+  if (in.rank == 2 && out.rank == 1 && in.strides[0] == 1 && si != 1 && in.extents[0] >= 32 && dt != GPUOS_I32 &&
+      cols > 0) {
+    switch (dt) {
+      case GPUOS_F32: reduce_rows_by_thread<MODE, GPUOS_F32>(in, out, in.extents[0], cols, c); break;
+      case GPUOS_F64: reduce_rows_by_thread<MODE, GPUOS_F64>(in, out, in.extents[0], cols, c); break;
+      case GPUOS_F16: reduce_rows_by_thread<MODE, GPUOS_F16>(in, out, in.extents[0], cols, c); break;
+      default: reduce_rows_by_thread<MODE, GPUOS_BF16>(in, out, in.extents[0], cols, c); break;
+    }
+    return GPUOS_OK;
+  }
   RowIter it;
   it.init(in);
+  if (MODE == 0 && si == 1 && cols <= 512 && dt != GPUOS_I32) {
+    // short contiguous rows: 8-lane sub-units, four rows per warp in flight
+    // (a whole warp per row left most lanes idle and one row's latency per
+    // step); warp-uniform row rounds keep every shuffle convergent
+    RowSched rs;
+    rs.lane = c->tid & 7;
+    rs.width = 8;
+    int64_t lo, hi;
+    part_range(it.rows, c->part, c->nparts, 1, &lo, &hi);
+    const int sub = (c->tid & 31) >> 3, warp = c->tid >> 5, nw = c->nthreads >> 5;
+    for (int64_t base = lo + (int64_t)warp * 4; base < hi; base += (int64_t)nw * 4) {
+      const int64_t row = base + sub;
+      double sum = 0.0;
+      int64_t oo = 0;
+      if (row < hi) {
+        int64_t oi;
+        it.offsets(row, in.strides, out.strides, &oi, &oo);
+        const char* ib = (const char*)in.addr + oi * dtype_width(dt);
+        switch (dt) {
+          case GPUOS_F32: sum = lane_sum_vec<GPUOS_F32>(ib, cols, rs); break;
+          case GPUOS_F64: sum = lane_sum_vec<GPUOS_F64>(ib, cols, rs); break;
+          case GPUOS_F16: sum = lane_sum_vec<GPUOS_F16>(ib, cols, rs); break;
+          default: sum = lane_sum_vec<GPUOS_BF16>(ib, cols, rs); break;
+        }
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      if (row < hi && rs.lane == 0) store_any(dt, (char*)out.addr + oo * dtype_width(dt), 0, sum);
+    }
+    return GPUOS_OK;
+  }
   RowSched rs;
   rs.init(c, it.rows, cols);
   for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
@@ -378,11 +493,20 @@ __device__ __forceinline__ int reduce_body(const gpuos_task* t, const Ctx* c) {
         r = (double)(long long)unit_sum((double)s, rs, c, (double*)c->smem);
       } else {
         double s = 0.0;
-        switch (dt) {
-          case GPUOS_F32: s = lane_sum<GPUOS_F32>(ib, si, cols, rs); break;
-          case GPUOS_F64: s = lane_sum<GPUOS_F64>(ib, si, cols, rs); break;
-          case GPUOS_F16: s = lane_sum<GPUOS_F16>(ib, si, cols, rs); break;
-          default: s = lane_sum<GPUOS_BF16>(ib, si, cols, rs); break;
+        if (si == 1) {
+          switch (dt) {
+            case GPUOS_F32: s = lane_sum_vec<GPUOS_F32>(ib, cols, rs); break;
+            case GPUOS_F64: s = lane_sum_vec<GPUOS_F64>(ib, cols, rs); break;
+            case GPUOS_F16: s = lane_sum_vec<GPUOS_F16>(ib, cols, rs); break;
+            default: s = lane_sum_vec<GPUOS_BF16>(ib, cols, rs); break;
+          }
+        } else {
+          switch (dt) {
+            case GPUOS_F32: s = lane_sum<GPUOS_F32>(ib, si, cols, rs); break;
+            case GPUOS_F64: s = lane_sum<GPUOS_F64>(ib, si, cols, rs); break;
+            case GPUOS_F16: s = lane_sum<GPUOS_F16>(ib, si, cols, rs); break;
+            default: s = lane_sum<GPUOS_BF16>(ib, si, cols, rs); break;
+          }
         }
         r = unit_sum(s, rs, c, (double*)c->smem);
       }

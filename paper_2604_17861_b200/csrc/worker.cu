@@ -526,7 +526,9 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
       // returned, and the host writes a bank before it publishes the version
       // that selects it, so an entry read under version v sees v's bank.
       // Nearness uses the hint seen by the previous round.
-      const bool near = pos + j < hint_seen + 2;
+      // Belt and braces for the hint protocol (see the published-slot update
+      // below): every 64th idle round a far ticket polls too.
+      const bool near = pos + j < hint_seen + 2 || (spins & 63) == 63;
       uint32_t ready = 0;  // consecutive valid slots starting at j
       uint4 v = make_uint4(0, 0, 0, 0);
       uint64_t aux = 0;    // lane 1: version, 2: yield_every, 3: trace_on, 4: tail, 5: stop_pos, 6: hint
@@ -570,6 +572,16 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
         while (ready < (uint32_t)kMaxBatch && (vb >> (8 * ready)) & 1u) ++ready;
         if (ready == 0 && tb != 0 && lane == 0) atomicAdd((unsigned long long*)&S->torn_reads, 1ull);
         if (ready > 0) {
+          // A published slot proves the producer tail is past it.  The tail
+          // word read in the same round may be older (the two PCIe reads are
+          // unordered), so without this the hint could stall below the
+          // consumed tickets, leaving no ticket "near" and nobody polling --
+          // a stall seen once in a 10^6-task mixed stream.
+          const uint64_t past = pos + j + ready;
+          if (past > hint_seen) {
+            hint_seen = past;
+            if (lane == 0) atomicMax((unsigned long long*)&S->hint, (unsigned long long)past);
+          }
           const uint32_t tr0 = (uint32_t)shfl64(aux, 3);
           tr_last = tr0;
           const uint64_t t_seen = tr0 ? globaltimer() : 0;
@@ -1103,6 +1115,20 @@ __global__ void gpuos_clock_probe(const uint32_t* flag, uint64_t* out, int round
   }
 }
 
+// Lean per-op baseline: what a conventional CUDA program launches for one
+// dense f32 add -- four small parameters, no descriptor, no dynamic shared
+// memory, a grid sized to the op (bench.py's second per-op-launch arm).
+__global__ void __launch_bounds__(256) gpuos_lean_add_kernel(float* out, const float* a, const float* b, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nv = n / 4;
+  if (i < nv) {
+    const float4 x = reinterpret_cast<const float4*>(a)[i], y = reinterpret_cast<const float4*>(b)[i];
+    reinterpret_cast<float4*>(out)[i] = make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z),
+                                                    __fadd_rn(x.w, y.w));
+  }
+  for (int e = nv * 4 + i; e < n && i < 4; e += 4) out[e] = __fadd_rn(a[e], b[e]);
+}
+
 __global__ void gpuos_gen_init(DevState* S, uint64_t claim, uint64_t hint, uint64_t stop_pos) {
   S->claim = claim;
   S->hint = hint;
@@ -1164,6 +1190,7 @@ void load_all_kernels(int* worker_regs, size_t* worker_local) {
   }
   cudaFuncGetAttributes(&fa, gpuos_clock_probe);
   cudaFuncGetAttributes(&fa, gpuos_gen_init);
+  cudaFuncGetAttributes(&fa, gpuos_lean_add_kernel);
 }
 
 cudaError_t worker_occupancy(int* per_sm) {
@@ -1184,6 +1211,12 @@ cudaError_t launch_task(const gpuos_task* t, uint32_t kind, uint64_t aux, uint32
 
 cudaError_t launch_clock_probe(const uint32_t* flag, uint64_t* out, int rounds, cudaStream_t st) {
   gpuos_clock_probe<<<1, 1, 0, st>>>(flag, out, rounds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lean_add(float* out, const float* a, const float* b, int n, cudaStream_t st) {
+  const int nv = (n + 3) / 4;
+  gpuos_lean_add_kernel<<<(nv + 255) / 256, 256, 0, st>>>(out, a, b, n);
   return cudaGetLastError();
 }
 

@@ -567,6 +567,7 @@ class Runtime {
   }
   uint64_t inject_operator_at(uint32_t op_id, const std::string& template_name, std::span<const double> params = {},
                               DType dtype = DType::F32) {
+    NvtxRange nvtx_("gpuos::inject_operator_at");
     if (stopped_) throw Error(ErrorCode::RuntimeStopped, "inject after shutdown");
     if (op_id < kFirstInjectedId)
       throw Error(ErrorCode::OutOfRange, "injected ids start at " + std::to_string(kFirstInjectedId));
@@ -593,6 +594,7 @@ class Runtime {
     return op_id;
   }
   void kill_operator(uint32_t op_id) {
+    NvtxRange nvtx_("gpuos::kill_operator");
     if (stopped_) throw Error(ErrorCode::RuntimeStopped, "kill after shutdown");
     table_->kill(op_id);
     modules_by_id_.erase(op_id);  // killed injected ops leave the eligible set
@@ -618,6 +620,7 @@ class Runtime {
   /// gpuos::Error on compile/link/load failures; the op keeps running its
   /// program until the flip.
   void promote_native(uint32_t op_id) {
+    NvtxRange nvtx_("gpuos::promote_native");
     if (stopped_) throw Error(ErrorCode::RuntimeStopped, "promote after shutdown");
     auto it = modules_by_id_.find(op_id);
     if (it == modules_by_id_.end()) throw Error(ErrorCode::NotInstalled, "op " + std::to_string(op_id) + " is not injected");
@@ -701,11 +704,13 @@ class Runtime {
   /// does not block -- the worker that claims a later task waits on the
   /// device's processed count.  Lasts until the next fence() or wait_all().
   void fence() {
+    NvtxRange nvtx_("gpuos::fence");
     if (!chain_.empty()) flush_chain();
     fence_target_ = committed_tasks_;
     fence_on_ = true;
   }
   void wait_all() {
+    NvtxRange nvtx_("gpuos::wait_all");
     if (!chain_.empty()) flush_chain();
     const int rc = gpuos_ring_wait_processed(dev_, committed_tasks_);
     if (rc == 0) fence_on_ = false;  // everything before any fence is done
@@ -778,6 +783,7 @@ class Runtime {
 
   /// Drain, stop the worker kernel, release all buffers; idempotent.
   void shutdown() {
+    NvtxRange nvtx_("gpuos::shutdown");
     if (stopped_) return;
     flush_chain();
     wait_all();
@@ -986,6 +992,7 @@ class Runtime {
   bool retained(const ChainStep& st) const { return cells_->use_count(st.cell) > chain_handle_baseline_; }
 
   void flush_chain() {
+    NvtxRange nvtx_("gpuos::flush_chain");
     if (chain_.empty()) return;
     std::vector<ChainStep> steps = std::move(chain_);
     chain_.clear();

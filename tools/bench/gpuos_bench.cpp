@@ -12,6 +12,7 @@
 //                    kernel's lifetime on its own stream.
 //   1  per-op      : baseline (a), one cudaLaunchKernel of the same task body
 //                    per task, back to back on one stream; CUDA-event timed.
+//   3  lean per-op : a minimal dense f32 add kernel per task (gpuos_launch_lean_add)
 //   2  e2e         : like 0 but inputs start in pinned host memory and outputs
 //                    end there: chunked H2D copies, submits and per-chunk D2H
 //                    copies, pipelined, all inside the (host-clock) timed region.
@@ -244,6 +245,27 @@ int gb_step(void* h, int mode, double* out) {
     float ms = 0;
     check_abi(gpuos_event_sync(b->dev, b->ev[1]), "sync ev1");
     check_abi(gpuos_event_elapsed_ms(b->dev, b->ev[0], b->ev[1], &ms), "elapsed");
+    dev_ms = ms;
+    host_ms = t1 - t0;
+  } else if (mode == 3) {
+    // lean per-op baseline: a minimal add kernel per task (4 parameters, no
+    // descriptor, no dynamic shared memory, no table lookup, no lock)
+    const BufferPool::Buffer& ba = rt.pool().lookup(b->A.buffer);
+    const BufferPool::Buffer& bb = rt.pool().lookup(b->B.buffer);
+    const BufferPool::Buffer& bc = rt.pool().lookup(b->Cv.buffer);
+    check_abi(gpuos_event_record(b->dev, b->ev[2], b->lstream), "ev2");
+    const double t0 = now_ms();
+    for (int i = 0; i < b->n; ++i) {
+      const uint64_t off = static_cast<uint64_t>(i) * b->e * 4;
+      check_abi(gpuos_launch_lean_add(b->dev, static_cast<char*>(bc.data) + off, static_cast<char*>(ba.data) + off,
+                                      static_cast<char*>(bb.data) + off, b->e, b->lstream),
+                "lean launch");
+    }
+    check_abi(gpuos_event_record(b->dev, b->ev[3], b->lstream), "ev3");
+    check_abi(gpuos_stream_sync(b->dev, b->lstream), "sync");
+    const double t1 = now_ms();
+    float ms = 0;
+    check_abi(gpuos_event_elapsed_ms(b->dev, b->ev[2], b->ev[3], &ms), "elapsed");
     dev_ms = ms;
     host_ms = t1 - t0;
   } else {
