@@ -25,12 +25,14 @@ struct FAdd {
   static constexpr bool kF32 = true;
   __device__ __forceinline__ double operator()(const double* v) const { return __dadd_rn(v[0], v[1]); }
   __device__ __forceinline__ float f32(const float* v) const { return __fadd_rn(v[0], v[1]); }
+  __device__ __forceinline__ long long i64(const long long* v) const { return v[0] + v[1]; }
 };
 struct FMul {
   static constexpr int A = 2;
   static constexpr bool kF32 = true;
   __device__ __forceinline__ double operator()(const double* v) const { return __dmul_rn(v[0], v[1]); }
   __device__ __forceinline__ float f32(const float* v) const { return __fmul_rn(v[0], v[1]); }
+  __device__ __forceinline__ long long i64(const long long* v) const { return v[0] * v[1]; }
 };
 struct FRelu {
   static constexpr int A = 1;
@@ -38,6 +40,7 @@ struct FRelu {
   // v < 0 ? 0 : v keeps -0.0 and NaN (ops.hpp:188)
   __device__ __forceinline__ double operator()(const double* v) const { return v[0] < 0.0 ? 0.0 : v[0]; }
   __device__ __forceinline__ float f32(const float* v) const { return v[0] < 0.0f ? 0.0f : v[0]; }
+  __device__ __forceinline__ long long i64(const long long* v) const { return v[0] < 0 ? 0 : v[0]; }
 };
 template <class F, class = void>
 struct HasF32 {
@@ -58,6 +61,41 @@ template <int DT>
 struct F32Eval {
   static constexpr bool value = DT == GPUOS_F32 || DT == GPUOS_F16 || DT == GPUOS_BF16;
 };
+// I32 add/mul/relu in int64: |a + b| < 2^32 and |a * b| < 2^62 are exact,
+// and the reference's double result, when it fits int32, is that exact value
+// (an out-of-range double narrows to INT32_MIN, as the int64 check does).
+template <bool I, class A, class B>
+struct PickT {
+  typedef A type;
+};
+template <class A, class B>
+struct PickT<false, A, B> {
+  typedef B type;
+};
+template <int DT>
+struct FastEval {  // (no <type_traits>: NVRTC compiles this header for native injected ops)
+  static constexpr bool value = F32Eval<DT>::value || DT == GPUOS_I32;
+  typedef typename PickT<DT == GPUOS_I32, long long, float>::type CT;
+};
+template <int DT>
+__device__ __forceinline__ typename FastEval<DT>::CT to_ct(typename DT_<DT>::T v) {
+  if constexpr (DT == GPUOS_I32) return (long long)v;
+  else if constexpr (DT == GPUOS_F16) return __half2float(v);
+  else if constexpr (DT == GPUOS_BF16) return __bfloat162float(v);
+  else return (float)v;
+}
+template <int DT>
+__device__ __forceinline__ typename DT_<DT>::T from_ct(typename FastEval<DT>::CT v) {
+  if constexpr (DT == GPUOS_I32) return (v >= -2147483648LL && v <= 2147483647LL) ? (int32_t)v : (int32_t)0x80000000u;
+  else if constexpr (DT == GPUOS_F16) return __float2half_rn(v);
+  else if constexpr (DT == GPUOS_BF16) return __float2bfloat16_rn(v);
+  else return v;
+}
+template <int DT, class F>
+__device__ __forceinline__ typename FastEval<DT>::CT fast_eval(const F& f, const typename FastEval<DT>::CT* x) {
+  if constexpr (DT == GPUOS_I32) return f.i64(x);
+  else return f.f32(x);
+}
 template <int DT>
 __device__ __forceinline__ float to_f32(typename DT_<DT>::T v) {
   if constexpr (DT == GPUOS_F16) return __half2float(v);
@@ -126,11 +164,11 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
           T* eo = reinterpret_cast<T*>(&vo);
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
-              float x[A];
+            if constexpr (FastEval<DT>::value && HasF32<F>::value) {
+              typename FastEval<DT>::CT x[A];
 #pragma unroll
-              for (int k = 0; k < A; ++k) x[k] = to_f32<DT>(ev[k][j]);
-              eo[j] = from_f32<DT>(f.f32(x));
+              for (int k = 0; k < A; ++k) x[k] = to_ct<DT>(ev[k][j]);
+              eo[j] = from_ct<DT>(fast_eval<DT>(f, x));
             } else {
               double x[A];
 #pragma unroll
@@ -154,23 +192,24 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
     // lane shuffle -- measured slower here: 7.6-8.0M vs 13.8M config-2 tasks/s.)
     int64_t lo, hi;
     part_range(n, c->part, c->nparts, 1, &lo, &hi);
-    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+    if constexpr (FastEval<DT>::value && HasF32<F>::value) {
+      typedef typename FastEval<DT>::CT CT;
       constexpr int UE = 16;
       const int64_t step = (int64_t)c->nthreads * UE;
       for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
-        float x[UE][A];
+        CT x[UE][A];
 #pragma unroll
         for (int u = 0; u < UE; ++u) {
           const int64_t e = e0 + (int64_t)u * c->nthreads;
           if (e < hi) {
 #pragma unroll
-            for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + e));
+            for (int k = 0; k < A; ++k) x[u][k] = to_ct<DT>(__ldcg(in[k] + e));
           }
         }
 #pragma unroll
         for (int u = 0; u < UE; ++u) {
           const int64_t e = e0 + (int64_t)u * c->nthreads;
-          if (e < hi) out[e] = from_f32<DT>(f.f32(x[u]));
+          if (e < hi) out[e] = from_ct<DT>(fast_eval<DT>(f, x[u]));
         }
       }
       return;
@@ -220,23 +259,24 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
     int64_t st[1 + A];
 #pragma unroll
     for (int k = 0; k <= A; ++k) st[k] = s.st[k][0];
-    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+    if constexpr (FastEval<DT>::value && HasF32<F>::value) {
+      typedef typename FastEval<DT>::CT CT;
       constexpr int U1F = 16;
       const int64_t stepf = (int64_t)c->nthreads * U1F;
       for (int64_t e0 = lo + c->tid; e0 < hi; e0 += stepf) {
-        float x[U1F][A];
+        CT x[U1F][A];
 #pragma unroll
         for (int u = 0; u < U1F; ++u) {
           const int64_t e = e0 + (int64_t)u * c->nthreads;
           if (e < hi) {
 #pragma unroll
-            for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + e * st[1 + k]));
+            for (int k = 0; k < A; ++k) x[u][k] = to_ct<DT>(__ldcg(in[k] + e * st[1 + k]));
           }
         }
 #pragma unroll
         for (int u = 0; u < U1F; ++u) {
           const int64_t e = e0 + (int64_t)u * c->nthreads;
-          if (e < hi) out[e * st[0]] = from_f32<DT>(f.f32(x[u]));
+          if (e < hi) out[e * st[0]] = from_ct<DT>(fast_eval<DT>(f, x[u]));
         }
       }
       return;
@@ -271,7 +311,8 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
       st1[k] = s.st[k][1];
     }
     const FastDiv fd = s.fd[1];
-    if constexpr (F32Eval<DT>::value && HasF32<F>::value) {
+    if constexpr (FastEval<DT>::value && HasF32<F>::value) {
+      typedef typename FastEval<DT>::CT CT;
       // 32-bit offsets when every operand's span fits (config-2 views do)
       int64_t span = 0;
 #pragma unroll
@@ -305,19 +346,20 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
           const int64_t ntiles = (int64_t)((R + 31) / 32) * tcols;
           int64_t tlo, thi;
           part_range(ntiles, c->part, c->nparts, 1, &tlo, &thi);
-          float* tile = reinterpret_cast<float*>(c->smem) + (size_t)warp * A * 32 * 33;
+          T* tile = reinterpret_cast<T*>(c->smem) + (size_t)warp * A * 32 * 33;  // raw elements
           for (int64_t tt = tlo + warp; tt < thi; tt += nw) {
             const int q0 = (int)(tt / tcols) * 32, r0 = (int)(tt % tcols) * 32;
 #pragma unroll
             for (int k = 0; k < A; ++k) {
               if (!tr[k]) continue;
-              float v[32];
+              T v[32];
               const int q = q0 + lane;
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                v[i] = (q < R && r0 + i < C) ? to_f32<DT>(__ldcg(in[k] + (q * s0[1 + k] + (r0 + i) * s1[1 + k]))) : 0.f;
+                if (q < R && r0 + i < C) v[i] = __ldcg(in[k] + (q * s0[1 + k] + (r0 + i) * s1[1 + k]));
 #pragma unroll
-              for (int i = 0; i < 32; ++i) tile[(k * 32 + i) * 33 + lane] = v[i];
+              for (int i = 0; i < 32; ++i)
+                if (q < R && r0 + i < C) tile[(k * 32 + i) * 33 + lane] = v[i];
             }
             __syncwarp();
             const int r = r0 + lane;
@@ -325,11 +367,11 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
             for (int i = 0; i < 32; ++i) {
               const int q = q0 + i;
               if (q < R && r < C) {
-                float x[A];
+                CT x[A];
 #pragma unroll
                 for (int k = 0; k < A; ++k)
-                  x[k] = tr[k] ? tile[(k * 32 + lane) * 33 + i] : to_f32<DT>(__ldcg(in[k] + (q * s0[1 + k] + r * s1[1 + k])));
-                out[q * s0[0] + r] = from_f32<DT>(f.f32(x));
+                  x[k] = to_ct<DT>(tr[k] ? tile[(k * 32 + lane) * 33 + i] : __ldcg(in[k] + (q * s0[1 + k] + r * s1[1 + k])));
+                out[q * s0[0] + r] = from_ct<DT>(fast_eval<DT>(f, x));
               }
             }
             __syncwarp();
@@ -339,7 +381,7 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
         constexpr int U2F = 16;
         const int64_t stepf = (int64_t)c->nthreads * U2F;
         for (int64_t e0 = lo + c->tid; e0 < hi; e0 += stepf) {
-          float x[U2F][A];
+          CT x[U2F][A];
           int32_t oo[U2F];
 #pragma unroll
           for (int u = 0; u < U2F; ++u) {
@@ -348,13 +390,13 @@ __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, co
               const uint32_t q = fd.div((uint32_t)e), r = (uint32_t)e - q * fd.d;
               oo[u] = (int32_t)q * s0[0] + (int32_t)r * s1[0];
 #pragma unroll
-              for (int k = 0; k < A; ++k) x[u][k] = to_f32<DT>(__ldcg(in[k] + ((int32_t)q * s0[1 + k] + (int32_t)r * s1[1 + k])));
+              for (int k = 0; k < A; ++k) x[u][k] = to_ct<DT>(__ldcg(in[k] + ((int32_t)q * s0[1 + k] + (int32_t)r * s1[1 + k])));
             }
           }
 #pragma unroll
           for (int u = 0; u < U2F; ++u) {
             const int64_t e = e0 + (int64_t)u * c->nthreads;
-            if (e < hi) out[oo[u]] = from_f32<DT>(f.f32(x[u]));
+            if (e < hi) out[oo[u]] = from_ct<DT>(fast_eval<DT>(f, x[u]));
           }
         }
         return;

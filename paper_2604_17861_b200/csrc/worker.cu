@@ -826,6 +826,7 @@ struct FAddOrMul {  // one loop for both binary ops (one instantiation, one regi
     return mul ? __dmul_rn(v[0], v[1]) : __dadd_rn(v[0], v[1]);
   }
   __device__ __forceinline__ float f32(const float* v) const { return mul ? __fmul_rn(v[0], v[1]) : __fadd_rn(v[0], v[1]); }
+  __device__ __forceinline__ long long i64(const long long* v) const { return mul ? v[0] * v[1] : v[0] + v[1]; }
 };
 __device__ __forceinline__ bool dense_f32_inline(uint32_t kind, const gpuos_task* t, const Ctx* c) {
   if (kind > GPUOS_OP_MUL || !(c->flags & kPlanDenseSame) || t->views[0].dtype != GPUOS_F32 || t->n_inputs != 2)
