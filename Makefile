@@ -70,7 +70,7 @@ build/cpp/test_host: tests/cpp/test_host.cpp tests/cpp/check.hpp $(HOST_HDRS) $(
 
 # GPU-box probes (producer cost breakdown, finite worker generation for ncu,
 # task-body call cost, PCIe round-trip floor)
-probes: build/probe/submit_cost build/probe/profile_worker build/probe/body_bench build/probe/pingpong
+probes: build/probe/submit_cost build/probe/profile_worker build/probe/body_bench build/probe/pingpong build/probe/burst_probe
 build/probe/body_bench: tools/probe/body_bench.cu $(DEV_HDRS)
 	@mkdir -p build/probe
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Iinclude -I$(CSRC) -o $@ $<
