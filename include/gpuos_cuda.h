@@ -168,8 +168,16 @@ typedef struct gpuos_task {
   uint64_t reserved2[2];
 } gpuos_task;
 
-/* Completion cell (8 bytes in mapped pinned memory), written exactly once
- * with a system-scope release by whoever finished the task:
+/* Completion cell (8 bytes in mapped pinned memory), written exactly once by
+ * whoever finished the task.  On the worker path the completer issues a
+ * gpu-scope release fence (fence.release.gpu, one per run of finished tasks)
+ * and then a relaxed system-scope store of the word: outputs are in L2 -- the
+ * point the host's copy engine and managed-memory migration read from --
+ * before the word is posted.  A sys-scope fence is the formal PTX guarantee
+ * for a host-CPU observer; it measured +3 us on the depth-1 p50 (8.3 -> 11.3
+ * us) for no throughput change, so the gpu-scope fence is kept and this is
+ * the documented assumption.  The per-op path uses
+ * fence.acq_rel.sys.  Layout:
  *   bits 0..7 state (0 Pending, 1 Done, 2 Failed), bits 8..15 ErrorCode,
  *   bits 16..63 low 48 bits of the task seq.
  * Replaces HandleState (runtime.hpp:59-88). */
@@ -335,6 +343,20 @@ typedef struct gpuos_dense_task {
   uint64_t wait_target; /* GPUOS_FLAG_AFTER: processed count to wait for */
 } gpuos_dense_task;
 int gpuos_ring_submit_dense(gpuos_dev* dev, const gpuos_dense_task* task);
+/* Producer view of the ring for a header-side dense publisher: the caller's
+ * thread writes compact slots itself (gdev::ring_write_dense in
+ * include/gpuos_ring_format.h, the same code gpuos_ring_submit_dense runs),
+ * saving the library call and the descriptor hand-off per task.  Single
+ * producer: `reserve` is the cursor gpuos_ring_reserve/_submit_dense share. */
+typedef struct gpuos_ring_view {
+  char* ring;               /* cap x 128-byte slots (mapped pinned) */
+  uint64_t mask;            /* cap - 1 */
+  uint64_t cap;
+  uint64_t* reserve;        /* producer cursor */
+  uint64_t* tail;           /* published count, read by the device */
+  const uint32_t* trace_on; /* enqueue stamps wanted */
+} gpuos_ring_view;
+int gpuos_ring_view_get(gpuos_dev* dev, gpuos_ring_view* out);
 
 /* Monitoring snapshot; head <= tail always holds. */
 int gpuos_ring_peek(gpuos_dev* dev, gpuos_snapshot* out);

@@ -63,4 +63,41 @@ GPUOS_RING_FN void contiguous_strides4(const int32_t* ext, int rank, int32_t* st
   }
 }
 
+#if !defined(__CUDACC_RTC__)
+// Compact-slot publisher (host): reserve, encode, checksum, publish word last,
+// then the tail.  gpuos_ring_submit_dense and the runtime's inline dense path
+// both run this.  x86 TSO orders the write-back stores for the device's
+// coherent PCIe reads; a read interleaving with them fails the checksum.
+// (Streaming stores, which skip the read-for-ownership, measured 4x slower:
+// 210 vs 55 ns per task.)
+inline int ring_write_dense(const gpuos_ring_view& r, const gpuos_dense_task& t) {
+  const uint64_t p = *r.reserve;
+  uint64_t* dst = reinterpret_cast<uint64_t*>(r.ring + (p & r.mask) * kRingSlot);
+  if (__atomic_load_n(dst, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
+  *r.reserve = p + 1;
+  // the device freed upcoming slots over PCIe (invalidating their first line
+  // in the host caches): fetch one for writing well ahead of use
+  __builtin_prefetch(r.ring + ((p + 16) & r.mask) * kRingSlot, 1);
+  uint64_t w[kSlotWords];
+  w[1] = t.seq;
+  w[2] = (uint64_t)t.op_id | ((uint64_t)t.flags << 32) | ((uint64_t)t.n_inputs << 48) | ((uint64_t)t.n_scalars << 56);
+  w[3] = t.size;
+  w[4] = t.done_cell;
+  w[5] = (t.flags & GPUOS_FLAG_AFTER) ? t.wait_target : (*r.trace_on ? __builtin_ia32_rdtsc() : 0);
+  w[6] = kFmtCompact | ((uint64_t)t.dtype << 8) | ((uint64_t)t.rank << 16);
+  w[8] = (uint64_t)(uint32_t)t.extents[0] | ((uint64_t)(uint32_t)t.extents[1] << 32);
+  w[9] = (uint64_t)(uint32_t)t.extents[2] | ((uint64_t)(uint32_t)t.extents[3] << 32);
+  for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) w[10 + k] = k <= t.n_inputs ? t.addr[k] : 0;
+  __builtin_memcpy(&w[15], &t.scalar0, 8);
+  uint64_t h = ring_term(p + 1, 0);
+  for (uint32_t i = 1; i < kSlotWords; ++i)
+    if (i != 7) h += ring_term(w[i], i);
+  w[7] = h;
+  for (uint32_t i = 1; i < kSlotWords; ++i) dst[i] = w[i];
+  __atomic_store_n(&dst[0], p + 1, __ATOMIC_RELEASE);
+  __atomic_store_n(r.tail, p + 1, __ATOMIC_RELEASE);
+  return GPUOS_OK;
+}
+#endif
+
 }  // namespace gdev

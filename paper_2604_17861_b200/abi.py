@@ -99,7 +99,7 @@ assert C.sizeof(View) == 48 and C.sizeof(Task) == SLOT_BYTES and C.sizeof(Instr)
 EXPORTS = [
     "gpuos_abi_version", "gpuos_default_cfg", "gpuos_dev_open", "gpuos_dev_close", "gpuos_dev_alive",
     "gpuos_dev_stop", "gpuos_dev_start", "gpuos_dev_num_workers", "gpuos_dev_sm_count",
-    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_ring_submit_dense", "gpuos_event_done", "gpuos_jit_compile_object", "gpuos_jit_link_worker",
+    "gpuos_set_yield_every", "gpuos_dev_hold", "gpuos_dev_run_finite", "gpuos_ring_submit_dense", "gpuos_ring_view_get", "gpuos_event_done", "gpuos_jit_compile_object", "gpuos_jit_link_worker",
     "gpuos_dev_load_native", "gpuos_table_install_native", "gpuos_program_upload", "gpuos_dev_clock_offset", "gpuos_buf_alloc", "gpuos_buf_free",
     "gpuos_buf_lookup", "gpuos_buf_copy", "gpuos_buf_fill", "gpuos_buf_prefetch", "gpuos_view_bind", "gpuos_cells_alloc",
     "gpuos_ring_capacity", "gpuos_ring_reserve", "gpuos_ring_publish", "gpuos_ring_peek",
@@ -138,6 +138,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "gpuos_dev_hold": ([P, I], I),
         "gpuos_dev_run_finite": ([P, C.POINTER(C.c_float)], I),
         "gpuos_ring_submit_dense": ([P, P], I),
+        "gpuos_ring_view_get": ([P, P], I),
         "gpuos_event_done": ([P, P], I),
         "gpuos_jit_compile_object": ([C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t], I),

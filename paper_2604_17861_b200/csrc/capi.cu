@@ -974,34 +974,25 @@ int gpuos_ring_publish(gpuos_dev* d, uint64_t pos, const gpuos_task* task) {
   return GPUOS_OK;
 }
 
-int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
-  const uint64_t p = d->reserve;
-  uint64_t* dst = reinterpret_cast<uint64_t*>(d->ring + (p & d->mask) * gdev::kRingSlot);
-  if (__atomic_load_n(dst, __ATOMIC_ACQUIRE) != p) return GPUOS_QUEUE_FULL;
-  d->reserve = p + 1;
-  asm volatile("prefetchw (%0)" ::"r"(d->ring + ((p + 16) & d->mask) * gdev::kRingSlot));
-  uint64_t w[gdev::kSlotWords];
-  w[1] = t->seq;
-  w[2] = (uint64_t)t->op_id | ((uint64_t)t->flags << 32) | ((uint64_t)t->n_inputs << 48) |
-         ((uint64_t)t->n_scalars << 56);
-  w[3] = t->size;
-  w[4] = t->done_cell;
-  w[5] = (t->flags & GPUOS_FLAG_AFTER) ? t->wait_target : (d->shadow.trace_on ? __rdtsc() : 0);
-  w[6] = gdev::kFmtCompact | ((uint64_t)t->dtype << 8) | ((uint64_t)t->rank << 16);
-  w[8] = (uint64_t)(uint32_t)t->extents[0] | ((uint64_t)(uint32_t)t->extents[1] << 32);
-  w[9] = (uint64_t)(uint32_t)t->extents[2] | ((uint64_t)(uint32_t)t->extents[3] << 32);
-  for (int k = 0; k <= GPUOS_MAX_INPUTS; ++k) w[10 + k] = k <= t->n_inputs ? t->addr[k] : 0;
-  std::memcpy(&w[15], &t->scalar0, 8);
-  uint64_t h = gdev::ring_term(p + 1, 0);
-  for (uint32_t i = 1; i < gdev::kSlotWords; ++i)
-    if (i != 7) h += gdev::ring_term(w[i], i);
-  w[7] = h;
-  // (streaming stores, which skip the read-for-ownership, measured 4x slower
-  // here: 210 vs 55 ns per task)
-  for (uint32_t i = 1; i < gdev::kSlotWords; ++i) dst[i] = w[i];
-  __atomic_store_n(&dst[0], p + 1, __ATOMIC_RELEASE);
-  __atomic_store_n(d->tail, p + 1, __ATOMIC_RELEASE);
+static gpuos_ring_view ring_view_of(gpuos_dev* d) {
+  gpuos_ring_view r;
+  r.ring = d->ring;
+  r.mask = d->mask;
+  r.cap = d->cap;
+  r.reserve = &d->reserve;
+  r.tail = d->tail;
+  r.trace_on = &d->shadow.trace_on;
+  return r;
+}
+
+int gpuos_ring_view_get(gpuos_dev* d, gpuos_ring_view* out) {
+  if (!d || !out) return GPUOS_INTERNAL;
+  *out = ring_view_of(d);
   return GPUOS_OK;
+}
+
+int gpuos_ring_submit_dense(gpuos_dev* d, const gpuos_dense_task* t) {
+  return gdev::ring_write_dense(ring_view_of(d), *t);
 }
 
 static uint64_t sum_mirror(const gpuos_dev* d, const uint64_t* m) {

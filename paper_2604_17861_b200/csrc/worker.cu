@@ -752,6 +752,9 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
       }
       if (!near) {
         __nanosleep(64u << expn);
+        // (a short backoff for tickets near the hint did not narrow the pickup
+        // spread of a burst after idle, and polling the producer tail from
+        // those tickets congested PCIe: burst pickup 120 us, depth-1 p50 94 us)
         if (expn < K.backoff_max_exp) ++expn;
       }
     }
@@ -887,7 +890,11 @@ extern "C" __global__ void __maxnreg__(kWorkerRegs) gpuos_worker_kernel(DevState
       mbar_wait(&H->done_bar[k % kBufs], (k / kBufs) & 1);
       uint32_t n = 1;
       while (n < (uint32_t)kBufs && mbar_test(&H->done_bar[(k + n) % kBufs], ((k + n) / kBufs) & 1)) ++n;
+#ifdef GPUOS_COMPLETE_FENCE_SYS
+      asm volatile("fence.release.sys;" ::: "memory");
+#else
       asm volatile("fence.release.gpu;" ::: "memory");
+#endif
       uint32_t n_done = 0, n_failed = 0;
       for (uint32_t i = 0; i < n; ++i, ++k) {
         const int b = (int)(k % kBufs);

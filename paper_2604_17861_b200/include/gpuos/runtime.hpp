@@ -34,6 +34,7 @@
 
 #include "gpuos/bytecode.hpp"
 #include "gpuos/errors.hpp"
+#include "gpuos_ring_format.h"
 #include "gpuos/expr.hpp"
 #include "gpuos/opcompiler.hpp"
 #include "gpuos/ops.hpp"
@@ -434,6 +435,7 @@ class Runtime {
     c.telemetry = cfg_.telemetry_enabled ? 1u : 0u;
     c.flags = cfg_.device_buffers ? GPUOS_CFG_DEVICE_BUFFERS : 0u;
     check_abi(gpuos_dev_open(cfg_.device, &c, &dev_), "gpuos_dev_open");
+    check_abi(gpuos_ring_view_get(dev_, &ring_), "gpuos_ring_view_get");
     pool_ = std::make_unique<BufferPool>(dev_);
     table_ = std::make_unique<OperatorTable>(dev_);
     cells_ = new detail::CellPool(dev_);
@@ -1157,6 +1159,17 @@ class Runtime {
   /// in-range view of the output's dtype and shape, at most one scalar.  Goes
   /// straight into the ring's compact slot encoding; returns false (nothing
   /// published) when the call does not qualify or the ring is full.
+  // The dense slot is written on this thread (gdev::ring_write_dense, the code
+  // gpuos_ring_submit_dense runs inside the library) through the producer
+  // view fetched at construction: no library call per task.
+  int publish_dense_slot(const gpuos_dense_task& t) {
+#ifdef GPUOS_NO_INLINE_PUBLISH
+    return gpuos_ring_submit_dense(dev_, &t);
+#else
+    return gdev::ring_write_dense(ring_, t);
+#endif
+  }
+
   bool try_publish_dense(uint64_t op_id, std::span<const TensorView> inputs, const TensorView& output,
                          std::span<const double> scalars, uint32_t cell, uint64_t id, uint16_t flags, bool* full) {
     const size_t rank = output.rank();
@@ -1196,12 +1209,12 @@ class Runtime {
       t.addr[k] = reinterpret_cast<uint64_t>(static_cast<char*>(b->data) + v.offset * static_cast<int64_t>(w));
     }
     for (size_t k = inputs.size() + 1; k <= GPUOS_MAX_INPUTS; ++k) t.addr[k] = 0;
-    int rc = gpuos_ring_submit_dense(dev_, &t);
+    int rc = publish_dense_slot(t);
     if (rc == static_cast<int>(ErrorCode::QueueFull) && cfg_.queue_full_spin_ns) {
       const uint64_t t0 = monotonic_ns();
       do {
         _mm_pause();
-        rc = gpuos_ring_submit_dense(dev_, &t);
+        rc = publish_dense_slot(t);
       } while (rc == static_cast<int>(ErrorCode::QueueFull) && monotonic_ns() - t0 < cfg_.queue_full_spin_ns);
     }
     *full = rc == static_cast<int>(ErrorCode::QueueFull);
@@ -1324,6 +1337,7 @@ class Runtime {
   bool fusion_on_ = false;
   uint64_t next_id_ = 1;
   uint64_t committed_tasks_ = 0;
+  gpuos_ring_view ring_{};  // producer view for the inline dense publisher
   uint64_t fence_target_ = 0;  // committed_tasks_ at the last fence()
   bool fence_on_ = false;
   uint64_t next_injected_id_ = kFirstInjectedId;

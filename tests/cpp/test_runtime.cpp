@@ -894,6 +894,56 @@ TEST_CASE("fusion: fused chains equal the oracle applied step by step") {
   }
 }
 
+// The reference's producer-side TaskQueue API (queue.hpp:156-300) over the
+// device ring: acquire_slot / commit / peek / wait_for_processed, with the
+// persistent workers as the consumer (try_claim / mark_done on the device).
+TEST_CASE("TaskQueue producer API: acquire, commit, peek over the device ring") {
+  Runtime rt(small_config(64, 4));
+  const int64_t n = 1000;
+  auto x = rt.alloc_tensor(DType::F32, {n});
+  auto y = rt.alloc_tensor(DType::F32, {n});
+  std::vector<double> xv(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) xv[static_cast<size_t>(i)] = static_cast<double>(i % 17) - 8.0;
+  fill(rt, x, xv);
+  rt.wait_all();
+  TaskQueue q(rt.device());
+  CHECK(q.capacity() == 64);
+  const TaskQueue::Snapshot s0 = q.peek();
+  gpuos_task t;
+  std::memset(&t, 0, sizeof(t));
+  t.op_id = static_cast<uint32_t>(OpKind::Relu);
+  t.n_inputs = 1;
+  t.size = static_cast<uint64_t>(n);
+  const auto view_of = [&](const TensorView& v, gpuos_view* o) {
+    o->addr = reinterpret_cast<uint64_t>(rt.pool().lookup(v.buffer).data);
+    o->extents[0] = static_cast<int32_t>(n);
+    o->strides[0] = 1;
+    o->dtype = GPUOS_F32;
+    o->rank = 1;
+    o->status = GPUOS_VIEW_OK;
+  };
+  view_of(y, &t.views[0]);
+  view_of(x, &t.views[1]);
+  const int tasks = 200;  // > capacity: acquire_slot reports a full ring until workers free slots
+  uint64_t full = 0;
+  for (int i = 0; i < tasks; ++i) {
+    t.seq = 900000 + static_cast<uint64_t>(i);
+    std::optional<uint64_t> pos;
+    while (!(pos = q.acquire_slot())) ++full;
+    q.commit(*pos, t);
+  }
+  REQUIRE(q.wait_for_processed(s0.processed + tasks) == 0);
+  const TaskQueue::Snapshot s1 = q.peek();
+  CHECK(s1.tail - s0.tail == static_cast<uint64_t>(tasks));
+  CHECK(s1.processed == s1.head);
+  CHECK(s1.head == s1.tail);
+  const std::vector<double> got = read_all(rt, y);
+  uint64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) bad += got[static_cast<size_t>(i)] == std::max(0.0, xv[static_cast<size_t>(i)]) ? 0 : 1;
+  CHECK(bad == 0);
+  std::printf("  %d tasks through TaskQueue, %llu full-ring retries\n", tasks, (unsigned long long)full);
+}
+
 TEST_CASE("shutdown drains every committed task") {
   Runtime rt(small_config(1024, 0));
   auto x = rt.alloc_tensor(DType::F32, {256});
