@@ -158,58 +158,82 @@ constexpr int kSoftmaxRegs = 8;  // rows of <= 256 elements stay in registers
 // most |d| e^d 2^-24 <= 2.2e-8), the sum in fp64, and the normalisation is a
 // multiply by the fp64 reciprocal -- within the rel 1e-6 / 1-ulp rules of
 // ops.hpp:200-238's fp64 computation (tests/cases.py row_cases).
-template <int DT>
+// NR rows per warp in flight, REGS values per lane per row (cols <= 32 REGS):
+// a warp used to walk its rows one at a time, one memory latency per row
+// (config 3's 128 x 128 softmax tasks: 32 rows per warp, ~94 us per phase).
+// Every row is computed exactly as before (same per-lane values, same
+// shuffle order), so results are unchanged.
+template <int DT, int REGS, int NR>
 __device__ __noinline__ int softmax_rows_f(const gpuos_view& in, const gpuos_view& out, const RowIter& it,
                                            const RowSched& rs, int64_t cols, int64_t si, int64_t so) {
   typedef typename DT_<DT>::T T;
-  for (int64_t row = rs.lo + rs.unit; row < rs.hi; row += rs.nunits) {
-    int64_t oi, oo;
-    it.offsets(row, in.strides, out.strides, &oi, &oo);
-    const T* ib = (const T*)in.addr + oi;
-    T* ob = (T*)out.addr + oo;
-    float x[kSoftmaxRegs];
+  for (int64_t base = rs.lo + (int64_t)rs.unit * NR; base < rs.hi; base += (int64_t)rs.nunits * NR) {
+    const T* ib[NR];
+    T* ob[NR];
+    float x[NR][REGS];
 #pragma unroll
-    for (int i = 0; i < kSoftmaxRegs; ++i) {
-      const int64_t j = rs.lane + 32 * i;
-      x[i] = j < cols ? (float)DT_<DT>::gload(ib + j * si) : 0.0f;
+    for (int r = 0; r < NR; ++r) {
+      int64_t oi = 0, oo = 0;
+      if (base + r < rs.hi) it.offsets(base + r, in.strides, out.strides, &oi, &oo);
+      ib[r] = (const T*)in.addr + oi;
+      ob[r] = (T*)out.addr + oo;
     }
-    // (value, first index) maximum over the non-NaN elements
-    float mv = 0.0f;
-    int mi = -1;
 #pragma unroll
-    for (int i = 0; i < kSoftmaxRegs; ++i) {
-      const int j = rs.lane + 32 * i;
-      if (j < cols && x[i] == x[i] && (mi < 0 || mv < x[i])) {
-        mv = x[i];
-        mi = j;
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int i = 0; i < REGS; ++i) {
+        const int64_t j = rs.lane + 32 * i;
+        x[r][i] = (base + r < rs.hi && j < cols) ? (float)DT_<DT>::gload(ib[r] + j * si) : 0.0f;
       }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
-      const int oi2 = __shfl_xor_sync(0xffffffffu, mi, o);
-      if (oi2 >= 0 && (mi < 0 || mv < ov || (!(ov < mv) && oi2 < mi))) {
-        mv = ov;
-        mi = oi2;
+    for (int r = 0; r < NR; ++r) {
+      if (base + r >= rs.hi) break;  // warp-uniform
+      // (value, first index) maximum over the non-NaN elements
+      float mv = 0.0f;
+      int mi = -1;
+#pragma unroll
+      for (int i = 0; i < REGS; ++i) {
+        const int j = rs.lane + 32 * i;
+        if (j < cols && x[r][i] == x[r][i] && (mi < 0 || mv < x[r][i])) {
+          mv = x[r][i];
+          mi = j;
+        }
       }
-    }
-    const float x0 = __shfl_sync(0xffffffffu, x[0], 0);
-    const double mx = (x0 != x0) ? (double)x0 : (double)mv;
-    double sum = 0.0;
 #pragma unroll
-    for (int i = 0; i < kSoftmaxRegs; ++i) {
-      const int64_t j = rs.lane + 32 * i;
-      x[i] = j < cols ? expf((float)((double)x[i] - mx)) : 0.0f;
-      sum += (double)x[i];
-    }
-    const double inv = __drcp_rn(warp_sum(sum));
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
+        const int oi2 = __shfl_xor_sync(0xffffffffu, mi, o);
+        if (oi2 >= 0 && (mi < 0 || mv < ov || (!(ov < mv) && oi2 < mi))) {
+          mv = ov;
+          mi = oi2;
+        }
+      }
+      const float x0 = __shfl_sync(0xffffffffu, x[r][0], 0);
+      const double mx = (x0 != x0) ? (double)x0 : (double)mv;
+      double sum = 0.0;
 #pragma unroll
-    for (int i = 0; i < kSoftmaxRegs; ++i) {
-      const int64_t j = rs.lane + 32 * i;
-      if (j < cols) DT_<DT>::store(ob + j * so, (double)x[i] * inv);
+      for (int i = 0; i < REGS; ++i) {
+        const int64_t j = rs.lane + 32 * i;
+        x[r][i] = j < cols ? expf((float)((double)x[r][i] - mx)) : 0.0f;
+        sum += (double)x[r][i];
+      }
+      const double inv = __drcp_rn(warp_sum(sum));
+#pragma unroll
+      for (int i = 0; i < REGS; ++i) {
+        const int64_t j = rs.lane + 32 * i;
+        if (j < cols) DT_<DT>::store(ob[r] + j * so, (double)x[r][i] * inv);
+      }
     }
   }
   return GPUOS_OK;
+}
+template <int DT>
+__device__ __forceinline__ int softmax_rows_dispatch(const gpuos_view& in, const gpuos_view& out, const RowIter& it,
+                                                     const RowSched& rs, int64_t cols, int64_t si, int64_t so) {
+  if (cols <= 32) return softmax_rows_f<DT, 1, 8>(in, out, it, rs, cols, si, so);
+  if (cols <= 64) return softmax_rows_f<DT, 2, 8>(in, out, it, rs, cols, si, so);
+  if (cols <= 128) return softmax_rows_f<DT, 4, 4>(in, out, it, rs, cols, si, so);
+  return softmax_rows_f<DT, 8, 2>(in, out, it, rs, cols, si, so);
 }
 __device__ __noinline__ int op_softmax(const gpuos_task* t, const Ctx* c) {
   if (t->n_inputs != 1) return GPUOS_ARITY_ERROR;
@@ -231,9 +255,9 @@ __device__ __noinline__ int op_softmax(const gpuos_task* t, const Ctx* c) {
   char* scratch = c->smem;
   if (rs.per_warp && cols <= 32 * kSoftmaxRegs && dt != GPUOS_F64) {
     switch (dt) {
-      case GPUOS_F32: return softmax_rows_f<GPUOS_F32>(in, out, it, rs, cols, si, so);
-      case GPUOS_F16: return softmax_rows_f<GPUOS_F16>(in, out, it, rs, cols, si, so);
-      default: return softmax_rows_f<GPUOS_BF16>(in, out, it, rs, cols, si, so);
+      case GPUOS_F32: return softmax_rows_dispatch<GPUOS_F32>(in, out, it, rs, cols, si, so);
+      case GPUOS_F16: return softmax_rows_dispatch<GPUOS_F16>(in, out, it, rs, cols, si, so);
+      default: return softmax_rows_dispatch<GPUOS_BF16>(in, out, it, rs, cols, si, so);
     }
   }
   // whole-group units visit identical rows, so their barriers stay matched

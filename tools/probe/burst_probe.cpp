@@ -60,6 +60,12 @@ int main(int argc, char** argv) {
       std::sort(v.begin(), v.end());
       return v.empty() ? std::make_pair(0.0, 0.0) : std::make_pair(v.front(), v.back());
     };
+    if (b == bursts - 1 && std::getenv("BURST_DETAIL")) {
+      std::sort(mine.begin(), mine.end(), [](auto& x, auto& y) { return x.seen_ns < y.seen_ns; });
+      for (auto& p : mine)
+        std::printf("  seq %llu worker %u ticket %.1f seen %.1f deq %.1f end %.1f done %.1f\n", (unsigned long long)p.seq,
+                    p.worker, us(p.ticket_ns), us(p.seen_ns), us(p.dequeue_ns), us(p.end_ns), us(p.done_ns));
+    }
     const auto a = mm(seen), d = mm(deq), e = mm(end), f = mm(done);
     std::printf("burst %d: %zu traced | submit %.1f us | seen %.1f..%.1f | deq %.1f..%.1f | end %.1f..%.1f | done "
                 "%.1f..%.1f | host waited %.1f us\n",
