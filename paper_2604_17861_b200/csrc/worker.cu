@@ -507,6 +507,22 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
         nb = pre_nb;
       } else {
         while (*(volatile uint32_t*)&S->hold) __nanosleep(2000);
+        // Lazy claiming: take a ticket only when the claim cursor is within
+        // two of the hint (this fetcher becomes one of the frontier pollers)
+        // or the hint says published work lies past the cursor.  Idle workers
+        // used to each hold a far ticket and reach it only as the hint crept
+        // forward hop by hop; a 32-task burst after idle was picked up in
+        // waves 16 us apart (tools/probe/burst_probe).  Now whoever wakes
+        // first claims work the hint has already announced.
+        for (uint32_t ns = 64;;) {
+          const uint64_t cl = ld_relaxed_gpu(&S->claim), hn = ld_relaxed_gpu(&S->hint);
+          if ((cl < hn + 2 || ld_relaxed_gpu(&S->stop_pos) != kRunning) && !*(volatile uint32_t*)&S->hold) {
+            hint_seen = hn > hint_seen ? hn : hint_seen;
+            break;
+          }
+          __nanosleep(ns);
+          if (ns < 1024) ns <<= 1;
+        }
         nb = hint_seen > last_pos + 2ull * K.num_workers ? (uint32_t)kMaxBatch : 1u;
         pos = atomicAdd((unsigned long long*)&S->claim, (unsigned long long)nb);
         last_pos = pos + nb - 1;
@@ -515,6 +531,7 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
     pre = false;
     pos = shfl64(pos, 0);
     nb = __shfl_sync(0xffffffffu, nb, 0);
+    hint_seen = shfl64(hint_seen, 0);
     uint32_t j = 0;  // next slot of the batch to hand over
     const uint64_t t_ticket = tr_last ? globaltimer() : 0;
     uint32_t spins = 0, expn = 0;
