@@ -36,6 +36,8 @@ with abi.Device(0, telemetry=True, num_workers=int(os.environ.get("LP_WORKERS", 
     a.write(np.ones(n, np.float32))
     b.write(np.ones(n, np.float32))
     va, vb, vc = (d.view(x.id, abi.F32, [n]) for x in (a, b, c))
+    if os.environ.get("LP_BCAST"):  # rank-0 broadcast second input: an extended slot, the general path
+        vb = d.view(b.id, abi.F32, [], [])
     lat = []
     for i in range(300):
         t = d.make_task(int(os.environ.get("LP_OP", abi.OP["add"])), vc, [va, vb])

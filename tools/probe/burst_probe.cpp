@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -36,7 +37,10 @@ int main(int argc, char** argv) {
       q.shape = o.shape = {S, D};
       q.strides = o.strides = {D, 1};
       q.offset = o.offset = int64_t{h} * S * D;
-      hs.push_back(rt.submit(OpKind::Mul, {q, s0}, o));
+      const int kind = std::getenv("BURST_KIND") ? std::atoi(std::getenv("BURST_KIND")) : 0;
+      if (kind == 0) hs.push_back(rt.submit(OpKind::Mul, {q, s0}, o));       // rank-0 broadcast (extended slot)
+      else if (kind == 1) hs.push_back(rt.submit(OpKind::Mul, {q, q}, o));   // dense (compact slot)
+      else hs.push_back(rt.submit(OpKind::Relu, {q}, o));                    // dense unary (compact slot)
     }
     const uint64_t t_sub = monotonic_ns();
     for (const TaskHandle& th : hs) th.wait();
