@@ -242,6 +242,106 @@ __device__ __forceinline__ void ew_dense(const gpuos_task* t, const Ctx* c, int6
   }
 }
 
+// One coalesced dimension with per-operand element strides st[0..A] (st[0]
+// the output's): stride-k views, rank-0 scalars, row-major views of any rank
+// that flatten to a single stride.  Offsets are e * stride; no divmod.
+template <int DT, class F>
+__device__ __forceinline__ void ew_rank1(const gpuos_task* t, const Ctx* c, int64_t n, F f, const int64_t* stp) {
+  typedef typename DT_<DT>::T T;
+  constexpr int A = F::A;
+  int64_t st[1 + A];  // in registers: through the pointer, every output store would force a reload
+#pragma unroll
+  for (int k = 0; k <= A; ++k) st[k] = stp[k];
+  T* out = (T*)t->views[0].addr;
+  const T* in[A];
+#pragma unroll
+  for (int k = 0; k < A; ++k) in[k] = (const T*)t->views[1 + k].addr;
+  int64_t lo, hi;
+  part_range(n, c->part, c->nparts, 1, &lo, &hi);
+  if constexpr (FastEval<DT>::value && HasF32<F>::value) {
+    typedef typename FastEval<DT>::CT CT;
+    constexpr int U1F = 16;
+    const int64_t stepf = (int64_t)c->nthreads * U1F;
+    for (int64_t e0 = lo + c->tid; e0 < hi; e0 += stepf) {
+      CT x[U1F][A];
+#pragma unroll
+      for (int u = 0; u < U1F; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) {
+#pragma unroll
+          for (int k = 0; k < A; ++k) x[u][k] = to_ct<DT>(__ldcg(in[k] + e * st[1 + k]));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U1F; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) out[e * st[0]] = from_ct<DT>(fast_eval<DT>(f, x[u]));
+      }
+    }
+  } else {
+    constexpr int U1 = 8;
+    const int64_t step = (int64_t)c->nthreads * U1;
+    for (int64_t e0 = lo + c->tid; e0 < hi; e0 += step) {
+      double x[U1][A];
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) {
+#pragma unroll
+          for (int k = 0; k < A; ++k) x[u][k] = DT_<DT>::gload(in[k] + e * st[1 + k]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const int64_t e = e0 + (int64_t)u * c->nthreads;
+        if (e < hi) DT_<DT>::store(out + e * st[0], f(x[u]));
+      }
+    }
+  }
+}
+
+// Register-resident broadcast check: the element stride of `in` against a
+// row-major dense output of the same rank-aligned shape when the view
+// flattens to one stride (every non-unit output dim d: stride_d == s *
+// out_stride_d), with s = 0 for a broadcast scalar.  Fixed-bound loops keep
+// everything in registers; the general Space build indexes small arrays at
+// run time, which lands in local memory -- measured 16,000 cycles of setup
+// for a 2,048-element broadcast half-task vs 2,000 for a dense one.
+__device__ __forceinline__ bool flat_stride(const gpuos_view& in, const gpuos_view& out, int64_t* s) {
+  const int ro = out.rank, ri = in.rank;
+  if (ri > ro) return false;
+  int64_t st = 0;
+  bool have = false, ok = true;
+#pragma unroll
+  for (int d = GPUOS_MAX_RANK - 1; d >= 0; --d) {
+    if (d < ro) {
+      const int di = d - (ro - ri);  // the input dim aligned with output dim d (right-aligned)
+      const int32_t eo = out.extents[d];
+      int32_t ei = 1, si = 0;
+#pragma unroll
+      for (int q = 0; q < GPUOS_MAX_RANK; ++q)
+        if (q == di) {
+          ei = in.extents[q];
+          si = in.strides[q];
+        }
+      if (di >= 0 && ei != eo && ei != 1) ok = false;  // incompatible: let the general path report it
+      const int64_t sd = (di >= 0 && ei == eo) ? si : 0;  // broadcast dims read stride 0
+      if (eo != 1) {
+        if (!have) {
+          // innermost non-unit dim: out stride there is the unit of the flat index
+          if (sd % out.strides[d] != 0) ok = false;
+          st = sd / out.strides[d];
+          have = true;
+        } else if (sd != st * out.strides[d]) {
+          ok = false;
+        }
+      }
+    }
+  }
+  *s = st;
+  return ok;
+}
+
 template <int DT, class F>
 __device__ __forceinline__ void ew_strided(const gpuos_task* t, const Ctx* c, const Space& s,
                                            int64_t n, F f) {
@@ -503,6 +603,25 @@ __device__ int ew_body(const gpuos_task* t, const Ctx* c, bool allow_int) {
   bool simple = dense_view(out);
   for (int k = 0; k < A && simple; ++k) simple = same_shape(t->views[1 + k], out) && dense_view(t->views[1 + k]);
   if (simple) return ew_dense_dispatch(t, c, out.dtype, n, f) ? GPUOS_OK : GPUOS_DTYPE_MISMATCH;
+  if (dense_view(out)) {
+    // every input flattens to one stride against the dense output (rank-0
+    // scalars, stride-k views, ...): the rank-1 loop, no iteration space
+    int64_t fs[1 + A];
+    fs[0] = 1;
+    bool flat = true;
+#pragma unroll
+    for (int k = 0; k < A; ++k) flat = flat && flat_stride(t->views[1 + k], out, &fs[1 + k]);
+    if (flat) {
+      switch (out.dtype) {
+        case GPUOS_F32: ew_rank1<GPUOS_F32>(t, c, n, f, fs); return GPUOS_OK;
+        case GPUOS_F64: ew_rank1<GPUOS_F64>(t, c, n, f, fs); return GPUOS_OK;
+        case GPUOS_I32: ew_rank1<GPUOS_I32>(t, c, n, f, fs); return GPUOS_OK;
+        case GPUOS_F16: ew_rank1<GPUOS_F16>(t, c, n, f, fs); return GPUOS_OK;
+        case GPUOS_BF16: ew_rank1<GPUOS_BF16>(t, c, n, f, fs); return GPUOS_OK;
+        default: return GPUOS_DTYPE_MISMATCH;
+      }
+    }
+  }
   Space s;
   build_space(s, out, A, st);
   switch (out.dtype) {
