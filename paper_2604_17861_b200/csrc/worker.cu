@@ -520,6 +520,9 @@ __device__ __forceinline__ void fetcher_main(DevState* S, WorkerHeader* H, uint3
             hint_seen = hn > hint_seen ? hn : hint_seen;
             break;
           }
+          // idle: keep the host-visible counts current (wait_all / peek read
+          // them; the completer updates H->done after this fetcher's last claim)
+          flush_mirror(K, w, F.mir, H->claimed, *(volatile uint64_t*)&H->done);
           __nanosleep(ns);
           if (ns < 1024) ns <<= 1;
         }
