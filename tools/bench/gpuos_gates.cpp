@@ -442,6 +442,21 @@ std::vector<Row> run_injection(const Spec& spec, Mode mode, uint64_t* inject_p50
 }
 
 // ---- contention: N submitters through a serializing front stage (bench.hpp:834-957) ----
+// Front stage of the contention workload: the reference's std::mutex, or
+// (diagnostic, --c8spin) a test-and-test-and-set spin lock, to separate the
+// runtime's own rate from the cost of a futex hand-off between 64 threads.
+struct SpinLock {
+  std::atomic<bool> f{false};
+  void lock() {
+    for (;;) {
+      if (!f.exchange(true, std::memory_order_acquire)) return;
+      while (f.load(std::memory_order_relaxed)) __builtin_ia32_pause();
+    }
+  }
+  void unlock() { f.store(false, std::memory_order_release); }
+};
+bool g_spin_front = false;
+
 std::vector<Row> run_contention(const Spec& spec, Mode m) {
   std::vector<Row> rows;
   const uint64_t tasks_total = spec.ops * spec.reps;
@@ -473,6 +488,7 @@ std::vector<Row> run_contention(const Spec& spec, Mode m) {
       fill_view(*rt, bs[s], bv[s]);
     }
     std::mutex front;  // one producer at a time: the runtime's threading contract
+    SpinLock spin;
     const bool serialize = N >= 1;
     std::vector<uint64_t> wait_ns(threads, 0);
     std::latch start(static_cast<std::ptrdiff_t>(threads + 1));
@@ -482,7 +498,12 @@ std::vector<Row> run_contention(const Spec& spec, Mode m) {
         start.arrive_and_wait();
         for (uint64_t t = 0; t < per_thread; ++t) {
           const uint64_t t0 = monotonic_ns();
-          if (serialize) {
+          if (serialize && g_spin_front) {
+            spin.lock();
+            wait_ns[s] += monotonic_ns() - t0;
+            rt->submit(OpKind::Add, {xs[s], bs[s]}, outs[s]);
+            spin.unlock();
+          } else if (serialize) {
             front.lock();
             wait_ns[s] += monotonic_ns() - t0;
             rt->submit(OpKind::Add, {xs[s], bs[s]}, outs[s]);
@@ -804,6 +825,11 @@ int main(int argc, char** argv) {
     if (w == "--c10") ok = gate_c10(golden) && ok;
     else if (w == "--c6") ok = gate_c6() && ok;
     else if (w == "--c8") ok = gate_c8() && ok;
+    else if (w == "--c8spin") {  // diagnostic: the C8 workload with a spin-lock front stage (not a gate)
+      g_spin_front = true;
+      gate_c8();
+      g_spin_front = false;
+    }
     else if (w == "--c9") ok = gate_c9() && ok;
     else if (w == "--attention") ok = gate_attention() && ok;
     else {
